@@ -1,0 +1,196 @@
+/*
+ * elis.h -- C ABI of the B200-native ISRTF re-predict + select hot path
+ * (ELIS, arXiv 2505.09142).  sm_100a only.  No CUDA or torch types in the
+ * signatures: device arrays are plain pointers, streams are `void*`
+ * (a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section in brackets).
+ *
+ * What the library computes:
+ *   Algorithm 1 (alg:scheduler_flow) lines 10-19: every job in the
+ *   Job Pool gets a priority from the predictor -- Predictor.init(job) on the
+ *   prompt, Predictor.iter(job) on "the prompt attached with the answer"
+ *    -- and the batcher forms "a batched prompt ... starting
+ *   with the prompt with the highest priority".  The predictor is a BGE
+ *   (BERT) encoder with mean pooling and eight FC layers, ReLU, hidden
+ *   1024 (P:359 [Sec. 4.2]); the priority is predicted remaining tokens
+ *   (Iterative SRTF, P:22, P:172-174 [Sec. 3.3]).
+ *
+ * Conventions for every call:
+ *   - Host-validated argument errors return immediately; nothing is enqueued.
+ *   - ELIS_OK means "enqueued on `stream`"; outputs are valid once the stream
+ *     reaches that point.  No call synchronises the host except
+ *     elis_sync_status, elis_iteration_host and elis_profile_read.
+ *   - Errors detected on the device (a token id >= vocab, a length outside
+ *     [1, max_position], sum(lengths) != total_tokens) are STICKY: they set a
+ *     device error word that elis_sync_status returns (and clears).
+ *   - The caller owns every array it passes; inputs must not alias outputs.
+ *     The predictor owns its device weights, workspaces and NCCL communicator.
+ *   - One predictor per device; calls on one predictor must be serialised by
+ *     the caller.  Several predictors may coexist.
+ *   - Determinism: identical inputs give bit-identical out_pred / out_ids.
+ */
+#ifndef ELIS_H_
+#define ELIS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ELIS_ABI_VERSION 1
+
+typedef enum {
+  ELIS_OK = 0,
+  ELIS_ERR_INVALID_ARG = 1,        /* bad pointer / size / enum value                  */
+  ELIS_ERR_CONFIG = 2,             /* elis_config inconsistent or unsupported shape   */
+  ELIS_ERR_UNSUPPORTED_DEVICE = 3, /* not compute capability 10.0 (B200, sm_100a)     */
+  ELIS_ERR_OOM = 4,                /* device allocation failed                        */
+  ELIS_ERR_CUDA = 5,               /* a CUDA runtime/driver call failed               */
+  ELIS_ERR_NCCL = 6,               /* an NCCL call failed                             */
+  ELIS_ERR_DEVICE_INPUT = 7        /* sticky device-detected input error (see above)  */
+} elis_status;
+
+typedef enum { ELIS_POOL_MEAN = 0, ELIS_POOL_CLS = 1 } elis_pooling;   /* P:359 / P:138 */
+typedef enum { ELIS_POLICY_ISRTF = 0, ELIS_POLICY_FCFS = 1 } elis_policy; /* P:22 / P:463 */
+
+/* Encoder + head shape.  BGE-base = {30522, 512, 2, 12, 768, 12, 3072}
+ * (P:121, P:123 [Sec. 3.1]); head = 8 layers, hidden 1024. */
+typedef struct {
+  int32_t abi_version;        /* must equal ELIS_ABI_VERSION                                  */
+  int32_t vocab_size;         /* 30522                                                        */
+  int32_t max_position;       /* 512 (max tokens per request)                                 */
+  int32_t type_vocab_size;    /* 2 (token type 0 is used everywhere)                          */
+  int32_t num_layers;         /* 12 base / 24 large / 2 tiny                                  */
+  int32_t hidden;             /* H: 768 / 1024 / 128; multiple of 128                         */
+  int32_t num_heads;          /* H / num_heads must be 32 or 64                               */
+  int32_t intermediate;       /* F: 4H; multiple of 128                                       */
+  float   ln_eps;             /* 1e-12                                                        */
+  int32_t pooling;            /* elis_pooling; default MEAN (reading R2)            */
+  int32_t head_layers;        /* 8                                              */
+  int32_t head_hidden;        /* 1024                                                 */
+  int32_t head_predicts_total;/* 0: the head emits remaining tokens (R4); 1: total*/
+  int32_t max_tokens;         /* workspace capacity: max sum(lengths) per predict call        */
+  int32_t max_requests;       /* workspace capacity: max n per predict / select call          */
+  int32_t device;             /* CUDA device ordinal                                          */
+} elis_config;
+
+typedef struct elis_predictor elis_predictor;
+
+int32_t elis_abi_version(void);
+
+/* Number of fp32 values the weight blob must hold for `cfg` (0 if cfg is invalid).
+ * Canonical order: HF BertModel state_dict (no pooler) --
+ *   embeddings.{word,position,token_type}_embeddings.weight, embeddings.LayerNorm.{weight,bias},
+ *   then per layer l: attention.self.{query,key,value}.{weight,bias},
+ *   attention.output.dense.{weight,bias}, attention.output.LayerNorm.{weight,bias},
+ *   intermediate.dense.{weight,bias}, output.dense.{weight,bias}, output.LayerNorm.{weight,bias}
+ * -- then head fc1..fc{head_layers} (weight [out, in] row-major, bias [out]).
+ * Linear weights are [out, in] row-major (nn.Linear).  Encoder matrices are
+ * converted to bf16 (round to nearest even) on upload; LN parameters, biases
+ * and the whole head stay fp32. */
+size_t elis_weight_count(const elis_config* cfg);
+
+/* Validate cfg, check the device is CC 10.0, upload + repack the weights
+ * (fused Wqkv [3H, H] bf16; head fp32), allocate workspaces for
+ * cfg->max_tokens / cfg->max_requests.  `weights` is a HOST array of
+ * `count` floats; it is copied (the caller may free it on return).
+ * Errors: INVALID_ARG (NULL / count mismatch), CONFIG, UNSUPPORTED_DEVICE, OOM, CUDA. */
+elis_status elis_predictor_create(const elis_config* cfg, const float* weights, size_t count,
+                                  elis_predictor** out);
+void elis_predictor_destroy(elis_predictor* p);
+
+/* Predictor.init / Predictor.iter for n requests at once (Alg. 1 lines 12/14).
+ *   tokens       DEVICE int32 [total_tokens], requests packed back to back; request i
+ *                starts at exclusive_scan(lengths)[i]; [CLS] first; token type 0.
+ *   lengths      DEVICE int32 [n], each in [1, max_position].
+ *   n            0 <= n <= max_requests (n = 0 is a no-op).
+ *   total_tokens == sum(lengths) <= max_tokens (checked on device: sticky error).
+ *   out_pred     DEVICE fp32: the head output y_i (remaining tokens, NOT clamped).
+ *   out_slot     optional DEVICE int32 [n]: if non-NULL, y_i is written to
+ *                out_pred[out_slot[i]] (scatter into an in-flight table), else out_pred[i].
+ * Per request: embedding + LN, num_layers post-LN BERT blocks over the request's own
+ * tokens (bidirectional, no cross-request attention), mean/CLS pooling, 8-FC head. */
+elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, const int32_t* lengths,
+                                   int32_t n, int64_t total_tokens, float* out_pred,
+                                   const int32_t* out_slot, void* stream);
+
+/* Preemption controls and tie-break inputs (P:345-348 [Backend Worker]). */
+typedef struct {
+  int32_t policy;            /* ELIS_POLICY_ISRTF or ELIS_POLICY_FCFS                               */
+  int32_t allow_preempt;     /* 1: running jobs may be displaced; 0: running jobs keep their slots   */
+  const uint32_t* order;     /* DEVICE [n] unique rank of (arrival, id); NULL => slot index          */
+  const uint8_t* running;    /* DEVICE [n] 1 if in the batch that just ran; NULL => none running     */
+  uint8_t* out_preempted;    /* DEVICE [n] running && !selected; NULL => not written                 */
+  int32_t* out_count;        /* DEVICE [1] number of ids written; NULL => not written                */
+  int32_t* out_nan_count;    /* DEVICE [1] NaN predictions seen (keyed as +inf); NULL => not written */
+} elis_preempt;
+
+/* Batcher.batch (Alg. 1 line 19): the batch_cap eligible slots with the
+ * smallest key (class, remaining, order), ascending.
+ *   remaining = pred (or pred - generated if cfg.head_predicts_total), fp32;
+ *   key = max(0, remaining), -0 -> +0, NaN -> +inf (lowest priority, counted);
+ *   FCFS: remaining ignored (arrival rank alone);
+ *   class = 0 for all slots if allow_preempt, else 0 for running slots and 1 for the rest.
+ *   pred       DEVICE fp32 [n]; generated DEVICE int32 [n] (< 0 marks an empty slot, never selected).
+ *   batch_cap  1 <= batch_cap <= 4096; n <= max(max_requests, 65536).
+ *   out_ids    DEVICE int32 [batch_cap], slot indices in priority order, -1 padded. */
+elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_t* generated,
+                              int32_t n, int32_t batch_cap, const elis_preempt* preempt,
+                              int32_t* out_ids, void* stream);
+
+/* ---- multi-GPU (BASELINE.json configs[4]) ------------------------------------------------
+ * One process per GPU.  The caller creates a 128-byte ncclUniqueId on rank 0
+ * (elis_nccl_unique_id) and broadcasts it (e.g. through torch.distributed). */
+elis_status elis_nccl_unique_id(void* out_id128);
+elis_status elis_dist_attach(elis_predictor* p, int32_t rank, int32_t world, const void* nccl_unique_id);
+/* Global ISRTF select over the union of every rank's slots.  Rank r owns global slots
+ * [global_offset, global_offset + n_local).  Each rank keys its slots, takes its local
+ * top-cap candidates, all-gathers them over NCCL (NVLink) and merges: the global top-cap
+ * is contained in the union of the local top-caps because keys are unique.
+ *   preempt->order must hold GLOBAL ranks (NULL => global slot index);
+ *   out_ids: DEVICE [batch_cap] GLOBAL slot indices, identical on every rank;
+ *   out_preempted (optional): this rank's n_local slots. */
+elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const int32_t* generated,
+                                   int32_t n_local, int32_t global_offset, int32_t batch_cap,
+                                   const elis_preempt* preempt, int32_t* out_ids, void* stream);
+
+/* ---- end-to-end convenience (HOST buffers) ----------------------------------------------
+ * One scheduling iteration from host memory: H2D copy of tokens/lengths/generated
+ * (+ order/running if given), predict, select, D2H copy of out_ids/out_count (and
+ * out_pred if non-NULL).  Synchronises `stream` before returning.  Pinned host memory
+ * gives asynchronous copies. */
+elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, const int32_t* h_lengths,
+                                int32_t n, int64_t total_tokens, const int32_t* h_generated,
+                                const uint32_t* h_order, const uint8_t* h_running, int32_t policy,
+                                int32_t allow_preempt, int32_t batch_cap, int32_t* h_out_ids,
+                                int32_t* h_out_count, float* h_out_pred, void* stream);
+
+/* Synchronise the stream of the last call and return (and clear) the sticky device
+ * error word: ELIS_ERR_DEVICE_INPUT if set, else ELIS_OK / ELIS_ERR_CUDA. */
+elis_status elis_sync_status(elis_predictor* p);
+/* Raw device error bits of the last elis_sync_status (1: token id out of range,
+ * 2: length outside [1, max_position], 4: sum(lengths) != total_tokens). */
+uint32_t elis_last_device_error_bits(elis_predictor* p);
+const char* elis_status_string(elis_status s);
+const char* elis_last_error(void);                 /* thread-local detail of the last failure */
+
+/* ---- instrumentation (bench / tests) ------------------------------------------------------ */
+/* Copy the final-layer fp32 hidden states [total_tokens, H] of the last predict call
+ * (DEVICE dst, `count` floats >= total_tokens * H) -- parity tests compare them with the oracle. */
+elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* stream);
+/* Number of kernels this predictor has launched so far. */
+uint64_t elis_launch_count(elis_predictor* p);
+/* Per-kernel-class CUDA-event timing on the launching stream.  enable=1 starts recording
+ * (resetting the totals); elis_profile_read synchronises, then fills up to `cap` entries:
+ * names[i] (static strings), total_ms[i], launches[i]; returns the number of classes. */
+elis_status elis_profile_enable(elis_predictor* p, int32_t enable);
+int32_t elis_profile_read(elis_predictor* p, const char** names, double* total_ms, int64_t* launches,
+                          int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELIS_H_ */

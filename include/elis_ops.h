@@ -1,0 +1,48 @@
+/*
+ * elis_ops.h -- per-kernel entry points of libelis, for parity tests and
+ * microbenchmarks.  Same conventions as elis.h (DEVICE pointers, `void*`
+ * stream, host-validated errors return before anything is enqueued).  bf16
+ * arrays are passed as raw uint16_t bit patterns.  These calls allocate and
+ * free their own small scratch (they synchronise `stream` when they do), so
+ * they are NOT for the hot path -- the predictor runs the same kernels.
+ */
+#ifndef ELIS_OPS_H_
+#define ELIS_OPS_H_
+
+#include "elis.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ELIS_EPI_BIAS_BF16 = 0,      /* out bf16 [M,N] = A W^T + bias                       (QKV, P:121 BERT) */
+  ELIS_EPI_BIAS_GELU_BF16 = 1, /* out bf16 [M,N] = GELU_erf(A W^T + bias)             (FFN1)            */
+  ELIS_EPI_BIAS_RESID_F32 = 2  /* out f32  [M,N] = A W^T + bias + residual (f32 [M,N]) (out-proj, FFN2)  */
+} elis_epilogue;
+
+/* tcgen05/TMEM/TMA GEMM.  A bf16 [M, K] row-major, W bf16 [N, K] row-major (nn.Linear),
+ * bias f32 [N]; M >= 1, N % 128 == 0, K % 64 == 0, all 16-byte aligned. */
+elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias, const float* residual,
+                         void* out, int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream);
+
+/* Varlen bidirectional multi-head attention ("process tokens in parallel").
+ * qkv bf16 [T, 3H] (Q | K | V, head h at columns h*d .. h*d+d-1 of each third),
+ * lengths int32 [n] (sum == T, each in [1, 512]); ctx bf16 [T, H] = per request i and head h:
+ * softmax(Q_h K_h^T / sqrt(d)) V_h over the request's own L_i tokens.  d = H / num_heads in {32, 64}. */
+elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T,
+                              int32_t hidden, int32_t num_heads, uint16_t* ctx, void* stream);
+
+/* Row LayerNorm: y = (u - mean) / sqrt(var + eps) * gamma + beta (population variance).
+ * u f32 [rows, H] -> out_f32 [rows, H] and (if non-NULL) out_bf16 [rows, H]; H in {128, 768, 1024}. */
+elis_status elis_op_layernorm(const float* u, const float* gamma, const float* beta, float eps,
+                              int64_t rows, int32_t H, float* out_f32, uint16_t* out_bf16, void* stream);
+
+/* Exact-fp32 FC layer of the regression head: Y f32 [n, N] = relu?(X f32 [n, K] W f32 [N, K]^T + b). */
+elis_status elis_op_fc_f32(const float* X, const float* W, const float* b, float* Y, int32_t n,
+                           int32_t N, int32_t K, int32_t relu, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELIS_OPS_H_ */

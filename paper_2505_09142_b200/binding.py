@@ -1,0 +1,239 @@
+"""Thin ctypes binding of libelis (include/elis.h, include/elis_ops.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  Device arrays are passed as raw pointers (``tensor.data_ptr()``),
+streams as ``torch.cuda.current_stream().cuda_stream``.  There is no CPU
+fallback: if the library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import inputs
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libelis.so")
+
+ELIS_OK = 0
+STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
+          6: "nccl", 7: "device input"}
+POLICY_ISRTF, POLICY_FCFS = 0, 1
+EPI_BIAS_BF16, EPI_BIAS_GELU_BF16, EPI_BIAS_RESID_F32 = 0, 1, 2
+
+_vp, _i32, _i64, _u32, _f32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                    ctypes.c_float, ctypes.c_size_t)
+
+
+class ElisConfig(ctypes.Structure):
+    _fields_ = [("abi_version", _i32), ("vocab_size", _i32), ("max_position", _i32), ("type_vocab_size", _i32),
+                ("num_layers", _i32), ("hidden", _i32), ("num_heads", _i32), ("intermediate", _i32),
+                ("ln_eps", _f32), ("pooling", _i32), ("head_layers", _i32), ("head_hidden", _i32),
+                ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32)]
+
+
+class ElisPreempt(ctypes.Structure):
+    _fields_ = [("policy", _i32), ("allow_preempt", _i32), ("order", _vp), ("running", _vp),
+                ("out_preempted", _vp), ("out_count", _vp), ("out_nan_count", _vp)]
+
+
+class ElisError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libelis.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ElisError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "elis_abi_version": (_i32, []),
+        "elis_weight_count": (_sz, [_vp]),
+        "elis_predictor_create": (_i32, [_vp, _vp, _sz, ctypes.POINTER(_vp)]),
+        "elis_predictor_destroy": (None, [_vp]),
+        "elis_predict_remaining": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
+        "elis_isrtf_select": (_i32, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+        "elis_nccl_unique_id": (_i32, [_vp]),
+        "elis_dist_attach": (_i32, [_vp, _i32, _i32, _vp]),
+        "elis_isrtf_select_dist": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+        "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
+                                       _vp, _vp]),
+        "elis_sync_status": (_i32, [_vp]),
+        "elis_last_device_error_bits": (_u32, [_vp]),
+        "elis_status_string": (ctypes.c_char_p, [_i32]),
+        "elis_last_error": (ctypes.c_char_p, []),
+        "elis_get_hidden": (_i32, [_vp, _vp, _i64, _vp]),
+        "elis_launch_count": (ctypes.c_uint64, [_vp]),
+        "elis_profile_enable": (_i32, [_vp, _i32]),
+        "elis_profile_read": (_i32, [_vp, _vp, _vp, _vp, _i32]),
+        "elis_op_gemm": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+        "elis_op_attention": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
+        "elis_op_layernorm": (_i32, [_vp, _vp, _vp, _f32, _i64, _i32, _vp, _vp, _vp]),
+        "elis_op_fc_f32": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(status: int, what: str = ""):
+    if status != ELIS_OK:
+        detail = lib().elis_last_error().decode(errors="replace")
+        raise ElisError(f"{what}: {STATUS.get(status, status)} ({detail})")
+
+
+def _ptr(t):
+    """Device/host pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
+                head_predicts_total: bool = False) -> ElisConfig:
+    return ElisConfig(1, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
+                      cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
+                      int(head_predicts_total), int(max_tokens), int(max_requests), int(device))
+
+
+class Predictor:
+    """Owner of one elis_predictor (device weights + workspaces)."""
+
+    def __init__(self, cfg: inputs.EncoderConfig, flat_weights: np.ndarray, max_tokens: int, max_requests: int,
+                 device: int = 0, head_predicts_total: bool = False):
+        L = lib()
+        self.cfg = cfg
+        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total)
+        flat = np.ascontiguousarray(flat_weights, dtype=np.float32)
+        need = L.elis_weight_count(ctypes.byref(self.c))
+        if need != flat.size:
+            raise ElisError(f"weight count {flat.size} != elis_weight_count {need}")
+        h = _vp()
+        check(L.elis_predictor_create(ctypes.byref(self.c), flat.ctypes.data, flat.size, ctypes.byref(h)),
+              "elis_predictor_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().elis_predictor_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- hot path
+    def predict_remaining(self, tokens, lengths, total_tokens: int, out_pred, out_slot=None, stream=None):
+        n = int(lengths.shape[0])
+        check(lib().elis_predict_remaining(self.h, _ptr(tokens), _ptr(lengths), n, int(total_tokens), _ptr(out_pred),
+                                           _ptr(out_slot), _stream(stream)), "elis_predict_remaining")
+
+    def isrtf_select(self, pred, generated, batch_cap: int, out_ids, policy=POLICY_ISRTF, allow_preempt=True,
+                     order=None, running=None, out_preempted=None, out_count=None, out_nan_count=None, stream=None):
+        pre = ElisPreempt(policy, int(allow_preempt), _ptr(order), _ptr(running), _ptr(out_preempted),
+                          _ptr(out_count), _ptr(out_nan_count))
+        check(lib().elis_isrtf_select(self.h, _ptr(pred), _ptr(generated), int(generated.shape[0]), int(batch_cap),
+                                      ctypes.byref(pre), _ptr(out_ids), _stream(stream)), "elis_isrtf_select")
+
+    def dist_attach(self, rank: int, world: int, unique_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(lib().elis_dist_attach(self.h, rank, world, buf), "elis_dist_attach")
+
+    def isrtf_select_dist(self, pred, generated, global_offset: int, batch_cap: int, out_ids, policy=POLICY_ISRTF,
+                          allow_preempt=True, order=None, running=None, out_preempted=None, out_count=None,
+                          out_nan_count=None, stream=None):
+        pre = ElisPreempt(policy, int(allow_preempt), _ptr(order), _ptr(running), _ptr(out_preempted),
+                          _ptr(out_count), _ptr(out_nan_count))
+        check(lib().elis_isrtf_select_dist(self.h, _ptr(pred), _ptr(generated), int(generated.shape[0]),
+                                           int(global_offset), int(batch_cap), ctypes.byref(pre), _ptr(out_ids),
+                                           _stream(stream)), "elis_isrtf_select_dist")
+
+    def iteration_host(self, tokens: np.ndarray, lengths: np.ndarray, generated: np.ndarray, batch_cap: int,
+                       out_ids: np.ndarray, out_count: np.ndarray | None = None, out_pred: np.ndarray | None = None,
+                       order: np.ndarray | None = None, running: np.ndarray | None = None, policy=POLICY_ISRTF,
+                       allow_preempt=True, stream=None):
+        """Host buffers in (numpy or pinned torch CPU tensors), ids out; synchronises."""
+        check(lib().elis_iteration_host(self.h, _ptr(tokens), _ptr(lengths), int(lengths.shape[0]),
+                                        int(tokens.shape[0]), _ptr(generated), _ptr(order), _ptr(running),
+                                        int(policy), int(allow_preempt), int(batch_cap), _ptr(out_ids),
+                                        _ptr(out_count), _ptr(out_pred), _stream(stream)), "elis_iteration_host")
+
+    # ---- instrumentation
+    def sync_status(self) -> int:
+        return lib().elis_sync_status(self.h)
+
+    def device_error_bits(self) -> int:
+        return lib().elis_last_device_error_bits(self.h)
+
+    def get_hidden(self, dst, stream=None):
+        check(lib().elis_get_hidden(self.h, _ptr(dst), int(dst.numel()), _stream(stream)), "elis_get_hidden")
+
+    def launch_count(self) -> int:
+        return int(lib().elis_launch_count(self.h))
+
+    def profile_enable(self, on: bool = True):
+        check(lib().elis_profile_enable(self.h, int(on)), "elis_profile_enable")
+
+    def profile_read(self) -> dict:
+        cap = 32
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_double * cap)()
+        cnt = (ctypes.c_int64 * cap)()
+        k = lib().elis_profile_read(self.h, names, ms, cnt, cap)
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(min(k, cap)) if cnt[i] > 0}
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().elis_nccl_unique_id(buf), "elis_nccl_unique_id")
+    return buf.raw
+
+
+# ---- per-op entry points (tests / microbenchmarks)
+def op_gemm(A, W, bias, out, epilogue: int, residual=None, stream=None):
+    M, K = A.shape
+    N = W.shape[0]
+    check(lib().elis_op_gemm(_ptr(A), _ptr(W), _ptr(bias), _ptr(residual), _ptr(out), M, N, K, epilogue,
+                             _stream(stream)), "elis_op_gemm")
+
+
+def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None):
+    check(lib().elis_op_attention(_ptr(qkv), _ptr(lengths), int(lengths.shape[0]), int(qkv.shape[0]), hidden,
+                                  num_heads, _ptr(ctx), _stream(stream)), "elis_op_attention")
+
+
+def op_layernorm(u, gamma, beta, eps: float, out32, outb=None, stream=None):
+    rows, H = u.shape
+    check(lib().elis_op_layernorm(_ptr(u), _ptr(gamma), _ptr(beta), eps, rows, H, _ptr(out32), _ptr(outb),
+                                  _stream(stream)), "elis_op_layernorm")
+
+
+def op_fc_f32(X, W, b, Y, relu: bool, stream=None):
+    n, K = X.shape
+    N = W.shape[0]
+    check(lib().elis_op_fc_f32(_ptr(X), _ptr(W), _ptr(b), _ptr(Y), n, N, K, int(relu), _stream(stream)),
+          "elis_op_fc_f32")

@@ -1,0 +1,726 @@
+// elis.cu -- host runtime behind the C ABI (include/elis.h, include/elis_ops.h).
+//
+// Owns the device weights (bf16 encoder matrices with Wq|Wk|Wv fused into one
+// [3H, H] operand, fp32 LN/bias/head), the workspace arena sized for
+// cfg.max_tokens / cfg.max_requests, the TMA descriptors of every encoder GEMM
+// (built once at create time: activation buffers never move), the NCCL
+// communicator and the instrumentation (launch counter, per-kernel CUDA-event
+// timing).  Every call enqueues on the caller's stream; nothing synchronises the
+// host except elis_sync_status / elis_iteration_host / elis_profile_read.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/elis.h"
+#include "../../include/elis_ops.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace elis;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+elis_status fail(elis_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+// NCCL is resolved at run time (dlopen), preferring a copy already loaded in the
+// process (torch's), so loading libelis never pins a second NCCL version.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+  api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+  api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+  api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString;
+  return api;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(ELIS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return static_cast<uint16_t>((u >> 16) | 0x40);  // NaN
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+bool config_valid(const elis_config* c, std::string* why) {
+  auto bad = [&](const char* m) { if (why) *why = m; return false; };
+  if (!c) return bad("cfg is NULL");
+  if (c->abi_version != ELIS_ABI_VERSION) return bad("abi_version mismatch");
+  if (c->vocab_size < 1 || c->max_position < 1 || c->max_position > 512 || c->type_vocab_size < 1)
+    return bad("vocab_size / max_position (<= 512) / type_vocab_size");
+  if (c->num_layers < 1) return bad("num_layers < 1");
+  if (c->hidden != 128 && c->hidden != 768 && c->hidden != 1024) return bad("hidden must be 128, 768 or 1024");
+  if (c->num_heads < 1 || c->hidden % c->num_heads) return bad("num_heads must divide hidden");
+  const int d = c->hidden / c->num_heads;
+  if (d != 32 && d != 64) return bad("head dim must be 32 or 64");
+  if (c->intermediate < 128 || c->intermediate % 128) return bad("intermediate must be a multiple of 128");
+  if (!(c->ln_eps > 0.f)) return bad("ln_eps must be > 0");
+  if (c->pooling != ELIS_POOL_MEAN && c->pooling != ELIS_POOL_CLS) return bad("pooling");
+  if (c->head_layers < 2 || c->head_hidden < 1) return bad("head_layers >= 2, head_hidden >= 1");
+  if (c->max_tokens < 1 || c->max_requests < 1) return bad("max_tokens / max_requests must be >= 1");
+  return true;
+}
+
+size_t weight_count_impl(const elis_config* c) {
+  const size_t H = c->hidden, F = c->intermediate, V = c->vocab_size, P = c->max_position, TV = c->type_vocab_size;
+  size_t n = V * H + P * H + TV * H + 2 * H;
+  n += static_cast<size_t>(c->num_layers) * (4 * (H * H + H) + 2 * H + (F * H + F) + (H * F + H) + 2 * H);
+  size_t in = H;
+  for (int j = 0; j < c->head_layers; ++j) {
+    const size_t out = (j == c->head_layers - 1) ? 1 : c->head_hidden;
+    n += out * in + out;
+    in = out;
+  }
+  return n;
+}
+
+struct Layer {
+  uint16_t *wqkv, *wo, *w1, *w2;
+  float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
+  GemmPlan p_qkv, p_out, p_ffn1, p_ffn2;
+};
+
+enum ProfClass {
+  PC_META, PC_EMBED, PC_QKV, PC_ATTN, PC_OUT, PC_LN, PC_FFN1, PC_FFN2, PC_POOL, PC_HEAD_FC, PC_HEAD_OUT,
+  PC_KEYS, PC_SELECT, PC_PREEMPT, PC_ALLGATHER, PC_COUNT
+};
+const char* kProfNames[PC_COUNT] = {"meta",        "embed_ln",   "gemm_qkv",    "attention", "gemm_out",
+                                    "layernorm",   "gemm_ffn1",  "gemm_ffn2",   "pool",      "head_fc",
+                                    "head_out",    "select_keys", "select_topk", "preempt",   "allgather"};
+
+}  // namespace
+
+struct elis_predictor {
+  elis_config cfg{};
+  int device = 0;
+  int num_sms = 148;
+  std::vector<void*> allocs;
+
+  uint16_t *word = nullptr, *pos = nullptr, *type0 = nullptr;
+  float *emb_g = nullptr, *emb_b = nullptr;
+  std::vector<Layer> layers;
+  std::vector<float*> head_w, head_b;
+  std::vector<int> head_dims;
+
+  // workspaces
+  float *h32 = nullptr, *u32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
+  uint16_t *hb = nullptr, *qkv = nullptr, *ctx = nullptr, *g = nullptr;
+  int32_t* cu = nullptr;
+  int2* work = nullptr;
+  int32_t* num_work = nullptr;
+  uint32_t* err = nullptr;
+  int64_t max_tiles = 0;
+
+  // select
+  int key_cap = 0;
+  SelectScratch sc{};
+  SelectScratch sc_merge{};
+  int32_t* tmp_ids = nullptr;
+
+  // dist
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  void *send = nullptr, *recv = nullptr;
+  unsigned long long* mkeys = nullptr;
+  int32_t* mids = nullptr;
+
+  // host-buffer iteration staging
+  int32_t *d_tokens = nullptr, *d_lengths = nullptr, *d_generated = nullptr, *d_ids = nullptr, *d_count = nullptr;
+  uint32_t* d_order = nullptr;
+  uint8_t* d_running = nullptr;
+  float* d_pred = nullptr;
+
+  // instrumentation
+  uint64_t launches = 0;
+  bool profiling = false;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  double prof_ms[PC_COUNT] = {};
+  int64_t prof_n[PC_COUNT] = {};
+
+  cudaStream_t last_stream = nullptr;
+  int64_t last_T = 0;
+  uint32_t last_err_bits = 0;
+
+  template <class T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) {
+      allocs.push_back(v);
+      cudaMemset(v, 0, std::max<size_t>(count, 1) * sizeof(T));
+    }
+    *p = static_cast<T*>(v);
+    return e;
+  }
+
+  cudaEvent_t next_event() {
+    if (event_next == event_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      event_pool.push_back(e);
+    }
+    return event_pool[event_next++];
+  }
+  void prof_begin(int cls, cudaStream_t st, cudaEvent_t* a) {
+    if (!profiling) return;
+    *a = next_event();
+    cudaEventRecord(*a, st);
+    (void)cls;
+  }
+  void prof_end(int cls, cudaStream_t st, cudaEvent_t a) {
+    if (!profiling) return;
+    cudaEvent_t b = next_event();
+    cudaEventRecord(b, st);
+    recs.push_back({cls, a, b});
+  }
+};
+
+// One kernel launch with accounting.  `expr` must return cudaError_t.
+#define LAUNCH(P, CLS, ST, expr)                                                      \
+  do {                                                                                \
+    cudaEvent_t _a = nullptr;                                                         \
+    (P)->prof_begin((CLS), (ST), &_a);                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return fail(ELIS_ERR_CUDA, std::string(kProfNames[CLS]) + ": " + cudaGetErrorString(_e)); \
+    (P)->prof_end((CLS), (ST), _a);                                                   \
+    (P)->launches += 1;                                                               \
+  } while (0)
+
+extern "C" {
+
+int32_t elis_abi_version(void) { return ELIS_ABI_VERSION; }
+
+size_t elis_weight_count(const elis_config* cfg) {
+  if (!config_valid(cfg, nullptr)) return 0;
+  return weight_count_impl(cfg);
+}
+
+const char* elis_status_string(elis_status s) {
+  switch (s) {
+    case ELIS_OK: return "ok";
+    case ELIS_ERR_INVALID_ARG: return "invalid argument";
+    case ELIS_ERR_CONFIG: return "invalid or unsupported config";
+    case ELIS_ERR_UNSUPPORTED_DEVICE: return "unsupported device (need CC 10.0, sm_100a)";
+    case ELIS_ERR_OOM: return "out of device memory";
+    case ELIS_ERR_CUDA: return "CUDA error";
+    case ELIS_ERR_NCCL: return "NCCL error";
+    case ELIS_ERR_DEVICE_INPUT: return "device-detected input error";
+  }
+  return "unknown status";
+}
+
+const char* elis_last_error(void) { return g_last_error.c_str(); }
+
+void elis_predictor_destroy(elis_predictor* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
+  for (void* a : p->allocs) cudaFree(a);
+  for (cudaEvent_t e : p->event_pool) cudaEventDestroy(e);
+  delete p;
+}
+
+elis_status elis_predictor_create(const elis_config* cfg, const float* weights, size_t count, elis_predictor** out) {
+  if (!out) return fail(ELIS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  std::string why;
+  if (!config_valid(cfg, &why)) return fail(ELIS_ERR_CONFIG, why);
+  if (!weights) return fail(ELIS_ERR_INVALID_ARG, "weights is NULL");
+  if (count != weight_count_impl(cfg)) return fail(ELIS_ERR_INVALID_ARG, "weight count mismatch");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev)
+    return fail(ELIS_ERR_UNSUPPORTED_DEVICE, "no such CUDA device");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, cfg->device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(ELIS_ERR_UNSUPPORTED_DEVICE, "compute capability " + std::to_string(prop.major) + "." +
+                                                 std::to_string(prop.minor) + " (need 10.0)");
+  CUDA_TRY(cudaSetDevice(cfg->device));
+
+  elis_predictor* p = new elis_predictor();
+  p->cfg = *cfg;
+  p->device = cfg->device;
+  p->num_sms = prop.multiProcessorCount;
+  const int H = cfg->hidden, F = cfg->intermediate, V = cfg->vocab_size, P = cfg->max_position;
+  const int64_t T = cfg->max_tokens;
+  const int N = cfg->max_requests;
+
+  auto cleanup_fail = [&](elis_status s, const std::string& m) {
+    elis_predictor_destroy(p);
+    return fail(s, m);
+  };
+#define ALLOC(ptr, cnt) \
+  if (p->alloc(&(ptr), (cnt)) != cudaSuccess) return cleanup_fail(ELIS_ERR_OOM, "cudaMalloc " #ptr)
+
+  // ---- weights: host repack then one upload per tensor
+  const float* w = weights;
+  auto take = [&](size_t n) { const float* r = w; w += n; return r; };
+  auto up_bf16 = [&](uint16_t* dst, const float* src, size_t n) {
+    std::vector<uint16_t> tmp(n);
+    for (size_t i = 0; i < n; ++i) tmp[i] = f32_to_bf16_rne(src[i]);
+    return cudaMemcpy(dst, tmp.data(), n * 2, cudaMemcpyHostToDevice);
+  };
+  auto up_f32 = [&](float* dst, const float* src, size_t n) {
+    return cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice);
+  };
+  ALLOC(p->word, static_cast<size_t>(V) * H);
+  ALLOC(p->pos, static_cast<size_t>(P) * H);
+  ALLOC(p->type0, H);
+  ALLOC(p->emb_g, H);
+  ALLOC(p->emb_b, H);
+  if (up_bf16(p->word, take(static_cast<size_t>(V) * H), static_cast<size_t>(V) * H) != cudaSuccess ||
+      up_bf16(p->pos, take(static_cast<size_t>(P) * H), static_cast<size_t>(P) * H) != cudaSuccess)
+    return cleanup_fail(ELIS_ERR_CUDA, "upload embeddings");
+  {
+    const float* tt = take(static_cast<size_t>(cfg->type_vocab_size) * H);
+    if (up_bf16(p->type0, tt, H) != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "upload type emb");
+  }
+  if (up_f32(p->emb_g, take(H), H) != cudaSuccess || up_f32(p->emb_b, take(H), H) != cudaSuccess)
+    return cleanup_fail(ELIS_ERR_CUDA, "upload emb LN");
+
+  p->layers.resize(cfg->num_layers);
+  for (int l = 0; l < cfg->num_layers; ++l) {
+    Layer& L = p->layers[l];
+    ALLOC(L.wqkv, static_cast<size_t>(3) * H * H);
+    ALLOC(L.bqkv, 3 * H);
+    ALLOC(L.wo, static_cast<size_t>(H) * H);
+    ALLOC(L.bo, H);
+    ALLOC(L.ln1g, H);
+    ALLOC(L.ln1b, H);
+    ALLOC(L.w1, static_cast<size_t>(F) * H);
+    ALLOC(L.b1, F);
+    ALLOC(L.w2, static_cast<size_t>(H) * F);
+    ALLOC(L.b2, H);
+    ALLOC(L.ln2g, H);
+    ALLOC(L.ln2b, H);
+    bool ok = true;
+    for (int j = 0; j < 3; ++j) {  // query, key, value -> rows [jH, (j+1)H) of Wqkv
+      ok &= up_bf16(L.wqkv + static_cast<size_t>(j) * H * H, take(static_cast<size_t>(H) * H),
+                    static_cast<size_t>(H) * H) == cudaSuccess;
+      ok &= up_f32(L.bqkv + j * H, take(H), H) == cudaSuccess;
+    }
+    ok &= up_bf16(L.wo, take(static_cast<size_t>(H) * H), static_cast<size_t>(H) * H) == cudaSuccess;
+    ok &= up_f32(L.bo, take(H), H) == cudaSuccess;
+    ok &= up_f32(L.ln1g, take(H), H) == cudaSuccess;
+    ok &= up_f32(L.ln1b, take(H), H) == cudaSuccess;
+    ok &= up_bf16(L.w1, take(static_cast<size_t>(F) * H), static_cast<size_t>(F) * H) == cudaSuccess;
+    ok &= up_f32(L.b1, take(F), F) == cudaSuccess;
+    ok &= up_bf16(L.w2, take(static_cast<size_t>(H) * F), static_cast<size_t>(H) * F) == cudaSuccess;
+    ok &= up_f32(L.b2, take(H), H) == cudaSuccess;
+    ok &= up_f32(L.ln2g, take(H), H) == cudaSuccess;
+    ok &= up_f32(L.ln2b, take(H), H) == cudaSuccess;
+    if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "upload layer weights");
+  }
+  int in = H;
+  for (int j = 0; j < cfg->head_layers; ++j) {
+    const int o = (j == cfg->head_layers - 1) ? 1 : cfg->head_hidden;
+    float *hw, *hbias;
+    ALLOC(hw, static_cast<size_t>(o) * in);
+    ALLOC(hbias, o);
+    if (up_f32(hw, take(static_cast<size_t>(o) * in), static_cast<size_t>(o) * in) != cudaSuccess ||
+        up_f32(hbias, take(o), o) != cudaSuccess)
+      return cleanup_fail(ELIS_ERR_CUDA, "upload head");
+    p->head_w.push_back(hw);
+    p->head_b.push_back(hbias);
+    p->head_dims.push_back(in);
+    in = o;
+  }
+  p->head_dims.push_back(1);
+
+  // ---- workspaces
+  ALLOC(p->h32, static_cast<size_t>(T) * H);
+  ALLOC(p->u32, static_cast<size_t>(T) * H);
+  ALLOC(p->hb, static_cast<size_t>(T) * H);
+  ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
+  ALLOC(p->ctx, static_cast<size_t>(T) * H);
+  ALLOC(p->g, static_cast<size_t>(T) * F);
+  ALLOC(p->cu, N + 1);
+  p->max_tiles = attn_max_tiles(T, N);
+  ALLOC(p->work, p->max_tiles);
+  ALLOC(p->num_work, 1);
+  ALLOC(p->err, 1);
+  ALLOC(p->pooled, static_cast<size_t>(N) * H);
+  ALLOC(p->z0, static_cast<size_t>(N) * cfg->head_hidden);
+  ALLOC(p->z1, static_cast<size_t>(N) * cfg->head_hidden);
+  p->key_cap = std::max(N, 65536);
+  ALLOC(p->sc.keys, p->key_cap);
+  ALLOC(p->sc.info, 8);
+  ALLOC(p->sc.sel_keys, kMaxBatchCap);
+  ALLOC(p->sc.sel_ids, kMaxBatchCap);
+  ALLOC(p->tmp_ids, kMaxBatchCap);
+  p->sc_merge = p->sc;
+  ALLOC(p->sc_merge.info, 8);
+  p->sc_merge.sel_keys = nullptr;
+  p->sc_merge.sel_ids = nullptr;
+
+  // ---- GEMM plans (TMA descriptors over the fixed workspaces; M set per call)
+  for (int l = 0; l < cfg->num_layers; ++l) {
+    Layer& L = p->layers[l];
+    bool ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
+              make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->u32, 0, H, H, EPI_BIAS_RESID_F32) &&
+              make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
+              make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->u32, 0, H, F, EPI_BIAS_RESID_F32);
+    if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "create sync");
+#undef ALLOC
+  *out = p;
+  return ELIS_OK;
+}
+
+elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
+                                   int64_t total_tokens, float* out_pred, const int32_t* out_slot, void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (n < 0 || n > p->cfg.max_requests) return fail(ELIS_ERR_INVALID_ARG, "n outside [0, max_requests]");
+  if (n == 0) return ELIS_OK;
+  if (!tokens || !lengths || !out_pred) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  if (total_tokens < n || total_tokens > p->cfg.max_tokens)
+    return fail(ELIS_ERR_INVALID_ARG, "total_tokens outside [n, max_tokens]");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  const elis_config& c = p->cfg;
+  const int H = c.hidden;
+  const int M = static_cast<int>(total_tokens);
+  p->last_stream = st;
+  p->last_T = total_tokens;
+
+  LAUNCH(p, PC_META, st, launch_meta(lengths, n, total_tokens, c.max_position, p->cu, p->work, p->num_work, p->err, st));
+  LAUNCH(p, PC_EMBED, st,
+         launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
+                         p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err, st));
+  const int64_t tiles = attn_max_tiles(total_tokens, n);
+  for (int l = 0; l < c.num_layers; ++l) {
+    Layer& L = p->layers[l];
+    L.p_qkv.M = L.p_out.M = L.p_ffn1.M = L.p_ffn2.M = M;
+    LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
+    LAUNCH(p, PC_ATTN, st, launch_attention(p->qkv, p->cu, p->work, p->num_work, tiles, H, c.num_heads, p->ctx, st));
+    LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));
+    LAUNCH(p, PC_LN, st, launch_layernorm(p->u32, L.ln1g, L.ln1b, c.ln_eps, total_tokens, H, p->h32, p->hb, st));
+    LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));
+    LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));
+    LAUNCH(p, PC_LN, st, launch_layernorm(p->u32, L.ln2g, L.ln2b, c.ln_eps, total_tokens, H, p->h32, p->hb, st));
+  }
+  LAUNCH(p, PC_POOL, st, launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
+  const float* x = p->pooled;
+  float* bufs[2] = {p->z0, p->z1};
+  const int nl = c.head_layers;
+  for (int j = 0; j < nl - 1; ++j) {
+    float* y = bufs[j & 1];
+    LAUNCH(p, PC_HEAD_FC, st, launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, st));
+    x = y;
+  }
+  LAUNCH(p, PC_HEAD_OUT, st,
+         launch_head_out(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot, st));
+  return ELIS_OK;
+}
+
+static elis_status validate_select(elis_predictor* p, const float* pred, const int32_t* generated, int32_t n,
+                                   int32_t batch_cap, const elis_preempt* pre, int32_t* out_ids) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (n < 0 || n > p->key_cap) return fail(ELIS_ERR_INVALID_ARG, "n outside [0, max(max_requests, 65536)]");
+  if (batch_cap < 1 || batch_cap > kMaxBatchCap) return fail(ELIS_ERR_INVALID_ARG, "batch_cap outside [1, 4096]");
+  if (!out_ids || (n > 0 && (!pred || !generated))) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  if (pre && pre->policy != ELIS_POLICY_ISRTF && pre->policy != ELIS_POLICY_FCFS)
+    return fail(ELIS_ERR_INVALID_ARG, "policy");
+  return ELIS_OK;
+}
+
+elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_t* generated, int32_t n,
+                              int32_t batch_cap, const elis_preempt* pre, int32_t* out_ids, void* stream) {
+  elis_status s = validate_select(p, pred, generated, n, batch_cap, pre, out_ids);
+  if (s != ELIS_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->last_stream = st;
+  const int policy = pre ? pre->policy : ELIS_POLICY_ISRTF;
+  const int allow = pre ? pre->allow_preempt : 1;
+  const uint32_t* order = pre ? pre->order : nullptr;
+  const uint8_t* running = pre ? pre->running : nullptr;
+  LAUNCH(p, PC_KEYS, st,
+         launch_make_keys(pred, generated, order, running, n, policy, allow, p->cfg.head_predicts_total, 0u,
+                          p->sc.keys, p->sc.info, st));
+  LAUNCH(p, PC_SELECT, st,
+         launch_select_topk(p->sc.keys, nullptr, n, batch_cap, out_ids, pre ? pre->out_count : nullptr,
+                            pre ? pre->out_nan_count : nullptr, p->sc, st));
+  if (pre && pre->out_preempted)
+    LAUNCH(p, PC_PREEMPT, st, launch_preempt_flags(p->sc.keys, running, n, p->sc.info, pre->out_preempted, st));
+  return ELIS_OK;
+}
+
+elis_status elis_nccl_unique_id(void* out_id128) {
+  if (!out_id128) return fail(ELIS_ERR_INVALID_ARG, "NULL id");
+  if (!nccl().ok) return fail(ELIS_ERR_NCCL, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  if (nccl().getUniqueId(&id) != ncclSuccess) return fail(ELIS_ERR_NCCL, "ncclGetUniqueId");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out_id128, &id, 128);
+  return ELIS_OK;
+}
+
+elis_status elis_dist_attach(elis_predictor* p, int32_t rank, int32_t world, const void* nccl_unique_id) {
+  if (!p || !nccl_unique_id) return fail(ELIS_ERR_INVALID_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ELIS_ERR_INVALID_ARG, "rank / world");
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!nccl().ok) return fail(ELIS_ERR_NCCL, "libnccl.so.2 not found");
+  if (p->comm) {
+    nccl().commDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, 128);
+  ncclResult_t r = nccl().commInitRank(&p->comm, world, id, rank);
+  if (r != ncclSuccess) return fail(ELIS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().getErrorString(r));
+  p->rank = rank;
+  p->world = world;
+  const size_t cand = 16;  // Candidate {u64 key, i32 id, i32 pad}
+  if (!p->send) {
+    if (p->alloc(reinterpret_cast<uint8_t**>(&p->send), cand * kMaxBatchCap) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "send buffer");
+  }
+  if (p->alloc(reinterpret_cast<uint8_t**>(&p->recv), cand * kMaxBatchCap * world) != cudaSuccess ||
+      p->alloc(&p->mkeys, static_cast<size_t>(kMaxBatchCap) * world) != cudaSuccess ||
+      p->alloc(&p->mids, static_cast<size_t>(kMaxBatchCap) * world) != cudaSuccess)
+    return fail(ELIS_ERR_OOM, "recv buffers");
+  return ELIS_OK;
+}
+
+elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const int32_t* generated, int32_t n_local,
+                                   int32_t global_offset, int32_t batch_cap, const elis_preempt* pre,
+                                   int32_t* out_ids, void* stream) {
+  elis_status s = validate_select(p, pred, generated, n_local, batch_cap, pre, out_ids);
+  if (s != ELIS_OK) return s;
+  if (!p->comm) return fail(ELIS_ERR_INVALID_ARG, "elis_dist_attach was not called");
+  if (global_offset < 0) return fail(ELIS_ERR_INVALID_ARG, "global_offset < 0");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->last_stream = st;
+  const int policy = pre ? pre->policy : ELIS_POLICY_ISRTF;
+  const int allow = pre ? pre->allow_preempt : 1;
+  const uint32_t* order = pre ? pre->order : nullptr;
+  const uint8_t* running = pre ? pre->running : nullptr;
+  // 1. local keys (order defaults to the GLOBAL slot index) and local top-cap candidates
+  LAUNCH(p, PC_KEYS, st,
+         launch_make_keys(pred, generated, order, running, n_local, policy, allow, p->cfg.head_predicts_total,
+                          static_cast<uint32_t>(global_offset), p->sc.keys, p->sc.info, st));
+  LAUNCH(p, PC_SELECT, st,
+         launch_select_topk(p->sc.keys, nullptr, n_local, batch_cap, p->tmp_ids, nullptr,
+                            pre ? pre->out_nan_count : nullptr, p->sc, st));
+  LAUNCH(p, PC_SELECT, st, launch_pack_candidates(p->sc, batch_cap, global_offset, p->send, st));
+  // 2. all-gather the world x cap candidates over NCCL (NVLink / NVSwitch)
+  {
+    cudaEvent_t a = nullptr;
+    p->prof_begin(PC_ALLGATHER, st, &a);
+    ncclResult_t r = nccl().allGather(p->send, p->recv, static_cast<size_t>(batch_cap) * 16, ncclUint8, p->comm, st);
+    if (r != ncclSuccess) return fail(ELIS_ERR_NCCL, std::string("ncclAllGather: ") + nccl().getErrorString(r));
+    p->prof_end(PC_ALLGATHER, st, a);
+  }
+  // 3. identical merge on every rank
+  const int total = batch_cap * p->world;
+  LAUNCH(p, PC_SELECT, st, launch_unpack_candidates(p->recv, total, p->mkeys, p->mids, st));
+  LAUNCH(p, PC_SELECT, st,
+         launch_select_topk(p->mkeys, p->mids, total, batch_cap, out_ids, pre ? pre->out_count : nullptr, nullptr,
+                            p->sc_merge, st));
+  if (pre && pre->out_preempted)
+    LAUNCH(p, PC_PREEMPT, st,
+           launch_preempt_flags(p->sc.keys, running, n_local, p->sc_merge.info, pre->out_preempted, st));
+  return ELIS_OK;
+}
+
+elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, const int32_t* h_lengths, int32_t n,
+                                int64_t total_tokens, const int32_t* h_generated, const uint32_t* h_order,
+                                const uint8_t* h_running, int32_t policy, int32_t allow_preempt, int32_t batch_cap,
+                                int32_t* h_out_ids, int32_t* h_out_count, float* h_out_pred, void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (n < 1 || n > p->cfg.max_requests) return fail(ELIS_ERR_INVALID_ARG, "n outside [1, max_requests]");
+  if (!h_tokens || !h_lengths || !h_generated || !h_out_ids) return fail(ELIS_ERR_INVALID_ARG, "NULL host array");
+  if (total_tokens < n || total_tokens > p->cfg.max_tokens) return fail(ELIS_ERR_INVALID_ARG, "total_tokens");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!p->d_tokens) {
+    const int N = p->cfg.max_requests;
+    if (p->alloc(&p->d_tokens, p->cfg.max_tokens) != cudaSuccess || p->alloc(&p->d_lengths, N) != cudaSuccess ||
+        p->alloc(&p->d_generated, N) != cudaSuccess || p->alloc(&p->d_order, N) != cudaSuccess ||
+        p->alloc(&p->d_running, N) != cudaSuccess || p->alloc(&p->d_pred, N) != cudaSuccess ||
+        p->alloc(&p->d_ids, kMaxBatchCap) != cudaSuccess || p->alloc(&p->d_count, 1) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "iteration staging");
+  }
+  CUDA_TRY(cudaMemcpyAsync(p->d_tokens, h_tokens, total_tokens * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(p->d_lengths, h_lengths, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(p->d_generated, h_generated, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st));
+  if (h_order) CUDA_TRY(cudaMemcpyAsync(p->d_order, h_order, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st));
+  if (h_running) CUDA_TRY(cudaMemcpyAsync(p->d_running, h_running, static_cast<size_t>(n), cudaMemcpyHostToDevice, st));
+  elis_status s = elis_predict_remaining(p, p->d_tokens, p->d_lengths, n, total_tokens, p->d_pred, nullptr, stream);
+  if (s != ELIS_OK) return s;
+  elis_preempt pre{};
+  pre.policy = policy;
+  pre.allow_preempt = allow_preempt;
+  pre.order = h_order ? p->d_order : nullptr;
+  pre.running = h_running ? p->d_running : nullptr;
+  pre.out_count = p->d_count;
+  s = elis_isrtf_select(p, p->d_pred, p->d_generated, n, batch_cap, &pre, p->d_ids, stream);
+  if (s != ELIS_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(h_out_ids, p->d_ids, static_cast<size_t>(batch_cap) * 4, cudaMemcpyDeviceToHost, st));
+  if (h_out_count) CUDA_TRY(cudaMemcpyAsync(h_out_count, p->d_count, 4, cudaMemcpyDeviceToHost, st));
+  if (h_out_pred) CUDA_TRY(cudaMemcpyAsync(h_out_pred, p->d_pred, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return ELIS_OK;
+}
+
+elis_status elis_sync_status(elis_predictor* p) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaStreamSynchronize(p->last_stream));
+  CUDA_TRY(cudaGetLastError());
+  uint32_t bits = 0;
+  CUDA_TRY(cudaMemcpy(&bits, p->err, 4, cudaMemcpyDeviceToHost));
+  p->last_err_bits = bits;
+  if (bits) {
+    CUDA_TRY(cudaMemset(p->err, 0, 4));
+    return fail(ELIS_ERR_DEVICE_INPUT, "device error bits " + std::to_string(bits));
+  }
+  return ELIS_OK;
+}
+
+uint32_t elis_last_device_error_bits(elis_predictor* p) { return p ? p->last_err_bits : 0u; }
+
+elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* stream) {
+  if (!p || !dst) return fail(ELIS_ERR_INVALID_ARG, "NULL argument");
+  const int64_t need = p->last_T * p->cfg.hidden;
+  if (count < need) return fail(ELIS_ERR_INVALID_ARG, "dst too small");
+  CUDA_TRY(cudaMemcpyAsync(dst, p->h32, need * 4, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+uint64_t elis_launch_count(elis_predictor* p) { return p ? p->launches : 0; }
+
+elis_status elis_profile_enable(elis_predictor* p, int32_t enable) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  p->profiling = enable != 0;
+  p->recs.clear();
+  p->event_next = 0;
+  for (int i = 0; i < PC_COUNT; ++i) { p->prof_ms[i] = 0; p->prof_n[i] = 0; }
+  return ELIS_OK;
+}
+
+int32_t elis_profile_read(elis_predictor* p, const char** names, double* total_ms, int64_t* launches, int32_t cap) {
+  if (!p) return -1;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (const auto& r : p->recs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      p->prof_ms[r.cls] += ms;
+      p->prof_n[r.cls] += 1;
+    }
+  }
+  p->recs.clear();
+  p->event_next = 0;
+  const int k = std::min<int>(cap, PC_COUNT);
+  for (int i = 0; i < k; ++i) {
+    if (names) names[i] = kProfNames[i];
+    if (total_ms) total_ms[i] = p->prof_ms[i];
+    if (launches) launches[i] = p->prof_n[i];
+  }
+  return PC_COUNT;
+}
+
+// ------------------------------------------------------------------------------------------ ops
+elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias, const float* residual, void* out,
+                         int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream) {
+  if (!A || !W || !bias || !out || M < 1 || N < 128 || N % 128 || K < 64 || K % 64 || epilogue < 0 || epilogue > 2)
+    return fail(ELIS_ERR_INVALID_ARG, "gemm arguments");
+  if (epilogue == ELIS_EPI_BIAS_RESID_F32 && !residual) return fail(ELIS_ERR_INVALID_ARG, "residual is NULL");
+  GemmPlan g;
+  if (!make_gemm_plan(&g, A, M, W, bias, residual, out, M, N, K, epilogue))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T, int32_t hidden,
+                              int32_t num_heads, uint16_t* ctx, void* stream) {
+  if (!qkv || !lengths || !ctx || n < 1 || T < n || num_heads < 1 || hidden % num_heads)
+    return fail(ELIS_ERR_INVALID_ARG, "attention arguments");
+  const int d = hidden / num_heads;
+  if (d != 32 && d != 64) return fail(ELIS_ERR_INVALID_ARG, "head dim");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = attn_max_tiles(T, n);
+  int32_t *cu = nullptr, *nw = nullptr;
+  int2* work = nullptr;
+  uint32_t* err = nullptr;
+  CUDA_TRY(cudaMalloc(&cu, (n + 1) * 4));
+  CUDA_TRY(cudaMalloc(&nw, 4));
+  CUDA_TRY(cudaMalloc(&err, 4));
+  CUDA_TRY(cudaMalloc(&work, tiles * sizeof(int2)));
+  CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, st));
+  CUDA_TRY(launch_attention(qkv, cu, work, nw, tiles, hidden, num_heads, ctx, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  uint32_t bits = 0;
+  cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);
+  cudaFree(cu);
+  cudaFree(nw);
+  cudaFree(err);
+  cudaFree(work);
+  if (bits) return fail(ELIS_ERR_DEVICE_INPUT, "lengths invalid");
+  return ELIS_OK;
+}
+
+elis_status elis_op_layernorm(const float* u, const float* gamma, const float* beta, float eps, int64_t rows,
+                              int32_t H, float* out_f32, uint16_t* out_bf16, void* stream) {
+  if (!u || !gamma || !beta || !out_f32 || rows < 0 || (H != 128 && H != 768 && H != 1024))
+    return fail(ELIS_ERR_INVALID_ARG, "layernorm arguments");
+  CUDA_TRY(launch_layernorm(u, gamma, beta, eps, rows, H, out_f32, out_bf16, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_fc_f32(const float* X, const float* W, const float* b, float* Y, int32_t n, int32_t N, int32_t K,
+                           int32_t relu, void* stream) {
+  if (!X || !W || !b || !Y || n < 0 || N < 1 || K < 1) return fail(ELIS_ERR_INVALID_ARG, "fc arguments");
+  CUDA_TRY(launch_fc_f32(X, W, b, Y, n, N, K, relu, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// kernels.cuh -- launch interfaces between the libelis host runtime and its kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace elis {
+
+enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2 };
+
+// Device error bits (sticky; see elis.h).
+enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u };
+
+// ---- GEMM (gemm.cu)
+struct GemmPlan {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  const float* bias;
+  const float* resid;
+  void* out;
+  int M, N, K, epi;
+};
+int gemm_block_n(int N);
+bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// A: [a_rows >= M, K] bf16 (rows M..a_rows-1 are read but their outputs are not stored)
+bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
+                    const float* resid, void* out, int M, int N, int K, int epi);
+cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st);
+
+// ---- varlen metadata / embedding / LayerNorm (norm.cu)
+constexpr int kAttnTileQ = 64;
+// lengths[n] -> cu_seqlens[n+1], attention work list (request, q0) and its size; validates.
+cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
+                        int2* work, int32_t* num_work, uint32_t* err, cudaStream_t st);
+cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
+                            int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
+                            const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
+                            uint16_t* hb, uint32_t* err, cudaStream_t st);
+cudaError_t launch_layernorm(const float* u, const float* gamma, const float* beta, float eps, int64_t rows, int H,
+                             float* out32, uint16_t* outb, cudaStream_t st);
+
+// ---- attention (attention.cu)
+// grid upper bound on the number of q-tiles for T tokens in n requests
+inline int64_t attn_max_tiles(int64_t T, int n) { return (T + kAttnTileQ - 1) / kAttnTileQ + n; }
+cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu_seqlens, const int2* work,
+                             const int32_t* num_work, int64_t max_tiles, int H, int num_heads, uint16_t* ctx,
+                             cudaStream_t st);
+
+// ---- pooling + regression head (head.cu)
+cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
+                        float* pooled, cudaStream_t st);
+cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,
+                          cudaStream_t st);
+cudaError_t launch_head_out(const float* Z, const float* w, const float* b, int n, int K, float* out_pred,
+                            const int32_t* out_slot, cudaStream_t st);
+
+// ---- ISRTF select (select.cu)
+constexpr int kMaxBatchCap = 4096;
+struct SelectScratch {
+  unsigned long long* keys;   // [n]
+  uint32_t* info;             // [8]: prefix lo/hi, mask lo/hi, count, n_elig, nan_count
+  unsigned long long* sel_keys;  // [cap] selected keys in order (UINT64_MAX padded)
+  int32_t* sel_ids;              // [cap]
+};
+cudaError_t launch_make_keys(const float* pred, const int32_t* generated, const uint32_t* order,
+                             const uint8_t* running, int n, int policy, int allow_preempt, int head_predicts_total,
+                             uint32_t order_offset, unsigned long long* keys, uint32_t* info, cudaStream_t st);
+// top-cap over keys[n]; ids (optional) map position -> id; writes out_ids / out_count / scratch
+cudaError_t launch_select_topk(const unsigned long long* keys, const int32_t* ids, int n, int cap,
+                               int32_t* out_ids, int32_t* out_count, int32_t* out_nan, SelectScratch sc,
+                               cudaStream_t st);
+cudaError_t launch_preempt_flags(const unsigned long long* keys, const uint8_t* running, int n, const uint32_t* info,
+                                 uint8_t* out_preempted, cudaStream_t st);
+cudaError_t launch_pack_candidates(const SelectScratch sc, int cap, int global_offset, void* send, cudaStream_t st);
+cudaError_t launch_unpack_candidates(const void* recv, int total, unsigned long long* keys, int32_t* ids,
+                                     cudaStream_t st);
+
+}  // namespace elis

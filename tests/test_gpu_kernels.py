@@ -1,0 +1,136 @@
+"""Per-kernel parity on the B200: each CUDA kernel (through the C ABI, elis_ops.h)
+against the oracle's per-op function on the same (bf16-representable) inputs.
+
+Tolerances are derived from the arithmetic:
+  * GEMM, bf16 out: fp32 accumulation then one bf16 rounding (rel 2^-8 = 3.9e-3);
+  * GEMM, fp32 out (+ residual): fp32 accumulation of K bf16 products (~K * 2^-24 rel);
+  * attention: P rounded to bf16 for the PV product, output rounded to bf16;
+  * LayerNorm / FC head: pure fp32.
+"""
+import numpy as np
+import pytest
+
+from paper_2505_09142_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def bf16_tensor(x: np.ndarray):
+    """bf16-representable fp32 numpy -> (torch bf16 on cuda, exact fp64 numpy copy)."""
+    x = inputs.round_to_bf16(np.asarray(x, np.float32))
+    return torch.from_numpy(x).to(torch.bfloat16).cuda(), x.astype(np.float64)
+
+
+def to_np(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("M", [1, 129, 300, 1000])
+@pytest.mark.parametrize("N,K", [(384, 128), (128, 128), (512, 128), (2304, 768), (768, 768), (3072, 768),
+                                 (768, 3072), (1024, 1024)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_gemm_tcgen05_parity(cuda_lib, M, N, K, epi):
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(M * 7 + N + K + epi)
+    A, A64 = bf16_tensor(rng.normal(0, 1, (M, K)))
+    W, W64 = bf16_tensor(rng.normal(0, 0.05, (N, K)))
+    b64 = rng.normal(0, 0.1, N).astype(np.float32)
+    bias = torch.from_numpy(b64).cuda()
+    ref = oenc.linear(A64, W64, b64.astype(np.float64))
+    if epi == 0:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        binding.op_gemm(A, W, bias, out, epi)
+        torch.cuda.synchronize()
+        got = to_np(out)
+        assert np.abs(got - ref).max() <= 4e-3 * np.abs(ref).max() + 1e-6
+        np.testing.assert_allclose(got, ref, rtol=8e-3, atol=2e-3)
+    elif epi == 1:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        binding.op_gemm(A, W, bias, out, epi)
+        torch.cuda.synchronize()
+        ref = oenc.gelu(ref)
+        np.testing.assert_allclose(to_np(out), ref, rtol=8e-3, atol=2e-3)
+    else:
+        res64 = rng.normal(0, 1, (M, N)).astype(np.float32)
+        res = torch.from_numpy(res64).cuda()
+        out = torch.empty(M, N, dtype=torch.float32, device="cuda")
+        binding.op_gemm(A, W, bias, out, epi, residual=res)
+        torch.cuda.synchronize()
+        ref = ref + res64.astype(np.float64)
+        np.testing.assert_allclose(to_np(out), ref, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("d,nh", [(64, 12), (32, 4), (64, 16)])
+def test_attention_varlen_parity(cuda_lib, d, nh):
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    H = d * nh
+    lengths = np.array([1, 2, 63, 64, 65, 130, 7, 512, 200, 33], dtype=np.int32)
+    T = int(lengths.sum())
+    rng = np.random.default_rng(d + nh)
+    qkv, qkv64 = bf16_tensor(rng.normal(0, 1.0, (T, 3 * H)))
+    ctx = torch.full((T, H), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lt = torch.from_numpy(lengths).cuda()
+    binding.op_attention(qkv, lt, H, nh, ctx)
+    torch.cuda.synchronize()
+    got = to_np(ctx)
+    starts = inputs.offsets(lengths)
+    for i, L in enumerate(lengths):
+        sl = slice(starts[i], starts[i + 1])
+        ref = oenc.attention(qkv64[sl, :H], qkv64[sl, H:2 * H], qkv64[sl, 2 * H:], nh)
+        err = np.abs(got[sl] - ref).max()
+        assert err < 2e-2, (i, int(L), err)
+
+
+def test_attention_single_token_is_v(cuda_lib):
+    """L = 1 closed form on the GPU: ctx = v (up to bf16 of a bf16 value: exact)."""
+    from paper_2505_09142_b200 import binding
+    H, nh = 768, 12
+    lengths = np.ones(5, np.int32)
+    rng = np.random.default_rng(3)
+    qkv, qkv64 = bf16_tensor(rng.normal(0, 1.0, (5, 3 * H)))
+    ctx = torch.empty(5, H, dtype=torch.bfloat16, device="cuda")
+    binding.op_attention(qkv, torch.from_numpy(lengths).cuda(), H, nh, ctx)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(to_np(ctx), qkv64[:, 2 * H:])
+
+
+@pytest.mark.parametrize("H", [128, 768, 1024])
+def test_layernorm_parity(cuda_lib, H):
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(H)
+    rows = 333
+    u = rng.normal(0.5, 3.0, (rows, H)).astype(np.float32)
+    g = (1 + rng.uniform(-0.1, 0.1, H)).astype(np.float32)
+    b = rng.normal(0, 0.02, H).astype(np.float32)
+    out = torch.empty(rows, H, device="cuda")
+    outb = torch.empty(rows, H, dtype=torch.bfloat16, device="cuda")
+    binding.op_layernorm(torch.from_numpy(u).cuda(), torch.from_numpy(g).cuda(), torch.from_numpy(b).cuda(),
+                         1e-12, out, outb)
+    torch.cuda.synchronize()
+    ref = oenc.layer_norm(u.astype(np.float64), g, b, 1e-12)
+    np.testing.assert_allclose(to_np(out), ref, rtol=0, atol=5e-6)
+    np.testing.assert_allclose(to_np(outb), ref, rtol=8e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("n,N,K", [(1, 1024, 768), (37, 1024, 1024), (256, 1024, 128), (300, 1000, 1024)])
+def test_fc_f32_parity(cuda_lib, n, N, K):
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(n + N + K)
+    X = rng.normal(0, 1, (n, K)).astype(np.float32)
+    W = (rng.normal(0, 1, (N, K)) * np.sqrt(2.0 / K)).astype(np.float32)
+    b = rng.normal(0, 0.1, N).astype(np.float32)
+    for relu in (0, 1):
+        Y = torch.empty(n, N, device="cuda")
+        binding.op_fc_f32(torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), Y,
+                          relu)
+        torch.cuda.synchronize()
+        ref = oenc.linear(X, W, b)
+        if relu:
+            ref = np.maximum(ref, 0)
+        np.testing.assert_allclose(to_np(Y), ref, rtol=2e-5, atol=2e-5)

@@ -1,0 +1,193 @@
+"""End-to-end parity of elis_predict_remaining (+ select) on the B200 against the fp64 oracle.
+
+Bars (BASELINE.json north_star): predictions within 1e-2 relative
+(rel_i = |p_gpu - p_oracle| / max(|p_oracle|, 1 token)), final-layer hidden states
+within 2e-2 absolute, ISRTF selections bit-exact given identical predictions.
+"""
+import numpy as np
+import pytest
+
+from paper_2505_09142_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+PRED_RTOL = 1e-2
+HIDDEN_ATOL = 2e-2
+
+
+def make_predictor(name, max_tokens, max_requests, pooling=inputs.POOL_MEAN, **kw):
+    from paper_2505_09142_b200 import binding
+    cfg = inputs.EncoderConfig(**{**inputs.CONFIGS[name].to_dict(), "pooling": pooling})
+    W = inputs.make_weights(cfg, seed=0)
+    flat = inputs.flatten_weights(cfg, W)
+    return cfg, W, binding.Predictor(cfg, flat, max_tokens, max_requests, **kw)
+
+
+def run_predict(pred, lengths, tokens, with_hidden=False):
+    T = int(lengths.sum())
+    tok = torch.from_numpy(tokens).cuda()
+    lt = torch.from_numpy(lengths).cuda()
+    out = torch.full((len(lengths),), float("nan"), device="cuda")
+    pred.predict_remaining(tok, lt, T, out)
+    hidden = None
+    if with_hidden:
+        hidden = torch.empty(T, pred.cfg.hidden, device="cuda")
+        pred.get_hidden(hidden)
+    assert pred.sync_status() == 0
+    return out.cpu().numpy(), (hidden.cpu().numpy() if hidden is not None else None)
+
+
+def rel_err(gpu, ref):
+    return np.abs(gpu.astype(np.float64) - ref) / np.maximum(np.abs(ref), 1.0)
+
+
+@pytest.mark.parametrize("pooling", [inputs.POOL_MEAN, inputs.POOL_CLS])
+def test_cfg1_tiny_full_parity_and_select(cuda_lib, pooling):
+    """BASELINE.json configs[0]: tiny encoder, 16 requests x 64 tokens, one ISRTF select
+    with batch_cap 4, vs FCFS."""
+    from oracle import head as ohead
+    from oracle.select import isrtf_select
+    cfg, W, P = make_predictor("tiny", 16 * 64, 16, pooling)
+    lengths = np.full(16, 64, np.int32)
+    tokens = inputs.make_tokens(lengths, seed=1)
+    gpu, hid = run_predict(P, lengths, tokens, with_hidden=True)
+    ref, hs = ohead.predict_with_hidden(tokens, lengths, W, cfg)
+    hidden_err = np.abs(hid.astype(np.float64) - np.concatenate(hs)).max()
+    assert hidden_err <= HIDDEN_ATOL, hidden_err
+    if pooling == inputs.POOL_MEAN:
+        assert rel_err(gpu, ref).max() <= PRED_RTOL, rel_err(gpu, ref).max()
+    else:
+        # CLS pooling: report error relative to the prediction spread
+        assert (np.abs(gpu - ref) / ref.std()).max() <= 5e-2
+    # selection: bit-exact vs the oracle on the GPU's own fp32 predictions
+    gen = np.zeros(16, np.int32)
+    running = np.zeros(16, np.uint8)
+    running[:4] = 1                                    # the FCFS batch ran last
+    for policy in (0, 1):
+        ids = torch.empty(4, dtype=torch.int32, device="cuda")
+        pre = torch.empty(16, dtype=torch.uint8, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+        P.isrtf_select(torch.from_numpy(gpu).cuda(), torch.from_numpy(gen).cuda(), 4, ids, policy=policy,
+                       running=torch.from_numpy(running).cuda(), out_preempted=pre, out_count=cnt)
+        o_ids, o_cnt, o_pre, _ = isrtf_select(gpu, gen, 4, policy, True, None, running)
+        np.testing.assert_array_equal(ids.cpu().numpy(), o_ids)
+        np.testing.assert_array_equal(pre.cpu().numpy(), o_pre)
+        assert int(cnt.item()) == o_cnt
+        if policy == 1:
+            assert list(ids.cpu().numpy()) == [0, 1, 2, 3]
+    P.close()
+
+
+def test_base_ragged_parity(cuda_lib):
+    """BGE-base, ragged lengths spanning several GEMM/attention tiles and ragged tails."""
+    from oracle import head as ohead
+    lengths = np.array([1, 7, 32, 63, 64, 65, 127, 128, 129, 300, 511, 512], dtype=np.int32)
+    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths))
+    tokens = inputs.make_tokens(lengths, seed=2)
+    gpu, hid = run_predict(P, lengths, tokens, with_hidden=True)
+    ref, hs = ohead.predict_with_hidden(tokens, lengths, W, cfg)
+    hidden_err = np.abs(hid.astype(np.float64) - np.concatenate(hs)).max()
+    r = rel_err(gpu, ref)
+    print(f"base ragged: hidden max abs err {hidden_err:.4g}, pred max rel err {r.max():.4g}")
+    assert hidden_err <= HIDDEN_ATOL
+    assert r.max() <= PRED_RTOL
+    P.close()
+
+
+def test_batch_invariance_bitwise(cuda_lib):
+    """pred_i is bitwise identical whether request i is encoded alone, in a batch, or in a
+    different batch order (row-independent GEMMs, per-request attention/pool/head)."""
+    lengths = np.array([40, 200, 64, 1, 511, 77, 129], dtype=np.int32)
+    tokens = inputs.make_tokens(lengths, seed=3)
+    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths))
+    full, _ = run_predict(P, lengths, tokens)
+    starts = inputs.offsets(lengths)
+    for i in (0, 3, 4):
+        alone, _ = run_predict(P, lengths[i:i + 1], tokens[starts[i]:starts[i + 1]])
+        assert alone[0] == full[i]
+    perm = np.array([6, 2, 0, 5, 1, 4, 3])
+    tok_p = np.concatenate([tokens[starts[i]:starts[i + 1]] for i in perm])
+    permuted, _ = run_predict(P, lengths[perm], tok_p)
+    np.testing.assert_array_equal(permuted, full[perm])
+    P.close()
+
+
+def test_out_slot_scatter(cuda_lib):
+    lengths = np.array([30, 50, 70], dtype=np.int32)
+    tokens = inputs.make_tokens(lengths, seed=4)
+    cfg, W, P = make_predictor("tiny", 150, 3)
+    ref, _ = run_predict(P, lengths, tokens)
+    table = torch.full((10,), -1.0, device="cuda")
+    slots = torch.tensor([7, 2, 5], dtype=torch.int32, device="cuda")
+    P.predict_remaining(torch.from_numpy(tokens).cuda(), torch.from_numpy(lengths).cuda(), 150, table, slots)
+    t = table.cpu().numpy()
+    assert t[7] == ref[0] and t[2] == ref[1] and t[5] == ref[2] and t[0] == -1.0
+    P.close()
+
+
+def test_device_input_errors_are_sticky(cuda_lib):
+    from paper_2505_09142_b200 import binding
+    lengths = np.array([10, 20], dtype=np.int32)
+    tokens = inputs.make_tokens(lengths, seed=5)
+    cfg, W, P = make_predictor("tiny", 64, 4)
+    bad = tokens.copy()
+    bad[3] = 40000                                    # >= vocab
+    out = torch.empty(2, device="cuda")
+    P.predict_remaining(torch.from_numpy(bad).cuda(), torch.from_numpy(lengths).cuda(), 30, out)
+    assert P.sync_status() == 7 and P.device_error_bits() & 1
+    assert P.sync_status() == 0                       # cleared after reporting
+    P.predict_remaining(torch.from_numpy(tokens).cuda(), torch.from_numpy(lengths).cuda(), 29, out)
+    assert P.sync_status() == 7 and P.device_error_bits() & 4   # sum(lengths) != total_tokens
+    badlen = np.array([10, 600], dtype=np.int32)
+    P.predict_remaining(torch.from_numpy(np.zeros(610, np.int32) + 1000).cuda(),
+                        torch.from_numpy(badlen).cuda(), 64, out)
+    assert P.sync_status() == 7 and P.device_error_bits() & 2
+    with pytest.raises(binding.ElisError):           # host-validated: total > max_tokens
+        P.predict_remaining(torch.from_numpy(tokens).cuda(), torch.from_numpy(lengths).cuda(), 65, out)
+    P.close()
+
+
+def test_iteration_host_matches_device_path(cuda_lib):
+    """elis_iteration_host (host buffers, copies inside) == device-pointer calls."""
+    from oracle.select import isrtf_select
+    L, gen, _ = inputs.trace_lengths(40, seed=6)
+    tokens = inputs.make_tokens(L, seed=6)
+    cfg, W, P = make_predictor("tiny", int(L.sum()), 40)
+    dev_pred, _ = run_predict(P, L, tokens)
+    ids = np.empty(8, np.int32)
+    cnt = np.empty(1, np.int32)
+    pr = np.empty(40, np.float32)
+    P.iteration_host(tokens, L, gen, 8, ids, cnt, pr)
+    np.testing.assert_array_equal(pr, dev_pred)
+    o_ids, o_cnt, _, _ = isrtf_select(pr, gen, 8)
+    np.testing.assert_array_equal(ids, o_ids)
+    assert cnt[0] == o_cnt
+    P.close()
+
+
+def test_cfg2_full_size_sampled_parity(cuda_lib):
+    """BASELINE.json configs[1] at full size in the bench's launch configuration
+    (BGE-base, 256 trace-shaped requests): sampled predictions vs the oracle, and the
+    ISRTF batch bit-exact on the GPU's predictions."""
+    from oracle import head as ohead
+    from oracle.select import isrtf_select
+    n = 256
+    L, gen, _ = inputs.trace_lengths(n, seed=0)
+    tokens = inputs.make_tokens(L, seed=0)
+    cfg, W, P = make_predictor("base", int(L.sum()), n)
+    gpu, _ = run_predict(P, L, tokens)
+    order = np.argsort(L)
+    sample = sorted(set(order[np.linspace(0, n - 1, 6).astype(int)].tolist()))  # stratified by length
+    ref = ohead.predict(tokens, L, W, cfg, requests=sample)
+    r = rel_err(gpu[sample], ref)
+    print("cfg2 sampled rel err", r.max(), "lengths", L[sample])
+    assert r.max() <= PRED_RTOL
+    assert np.isfinite(gpu).all()
+    for cap in (4, 256):
+        ids = torch.empty(cap, dtype=torch.int32, device="cuda")
+        P.isrtf_select(torch.from_numpy(gpu).cuda(), torch.from_numpy(gen).cuda(), cap, ids)
+        o_ids, _, _, _ = isrtf_select(gpu, gen, cap)
+        np.testing.assert_array_equal(ids.cpu().numpy(), o_ids)
+    P.close()

@@ -1,0 +1,87 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the headers
+declare, and its host-only logic (weight count, config validation) agrees with the
+input generator.  No compute calls (there is no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2505_09142_b200 import binding, inputs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    names = []
+    for h in ("elis.h", "elis_ops.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"\b(elis_[a-z0-9_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    L = binding.lib()
+    names = _declared_functions()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+
+
+def test_abi_version():
+    assert binding.lib().elis_abi_version() == 1
+
+
+@pytest.mark.parametrize("name", ["tiny", "base", "large"])
+def test_weight_count_matches_generator(name):
+    cfg = inputs.CONFIGS[name]
+    c = binding.make_config(cfg, 1024, 16)
+    assert binding.lib().elis_weight_count(ctypes.byref(c)) == inputs.weight_count(cfg)
+
+
+def test_invalid_configs_rejected():
+    L = binding.lib()
+    base = inputs.CONFIGS["base"]
+    for bad in (dict(hidden=100), dict(num_heads=5), dict(max_position=1024), dict(intermediate=100),
+                dict(max_tokens=0)):
+        c = binding.make_config(base, 1024, 16)
+        for k, v in bad.items():
+            setattr(c, k, v)
+        assert L.elis_weight_count(ctypes.byref(c)) == 0
+        h = ctypes.c_void_p()
+        w = np.zeros(4, np.float32)
+        assert L.elis_predictor_create(ctypes.byref(c), w.ctypes.data, 4, ctypes.byref(h)) == 2  # ELIS_ERR_CONFIG
+
+
+def test_create_validates_weight_count_and_device():
+    L = binding.lib()
+    c = binding.make_config(inputs.CONFIGS["tiny"], 1024, 16)
+    h = ctypes.c_void_p()
+    w = np.zeros(10, np.float32)
+    assert L.elis_predictor_create(ctypes.byref(c), w.ctypes.data, 10, ctypes.byref(h)) == 1  # count mismatch
+    n = L.elis_weight_count(ctypes.byref(c))
+    w = np.zeros(n, np.float32)
+    st = L.elis_predictor_create(ctypes.byref(c), w.ctypes.data, n, ctypes.byref(h))
+    import torch
+    if not torch.cuda.is_available():
+        assert st == 3  # ELIS_ERR_UNSUPPORTED_DEVICE: no device here
+        assert b"device" in L.elis_last_error()
+    else:
+        assert st == 0
+        L.elis_predictor_destroy(h)
+
+
+def test_status_strings():
+    L = binding.lib()
+    for s in range(8):
+        assert L.elis_status_string(s)
+
+
+def test_null_argument_errors_without_gpu():
+    L = binding.lib()
+    # NULL predictor: host-validated, returns immediately
+    assert L.elis_predict_remaining(None, None, None, 1, 1, None, None, None) == 1
+    assert L.elis_isrtf_select(None, None, None, 1, 1, None, None, None) == 1
+    assert L.elis_sync_status(None) == 1
