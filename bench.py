@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""bench.py -- ISRTF re-predict + select throughput on B200 (BASELINE.json metric).
+
+One step = one scheduling iteration of ELIS Algorithm 1 lines 10-19:
+re-encode every due request (prompt + partial response) with the BGE encoder,
+predict remaining tokens with the 8-FC head, and select the next batch (ISRTF,
+batch_cap) -- i.e. one elis_predict_remaining + one elis_isrtf_select[_dist].
+
+Default workload (N=1): BASELINE.json configs[1] -- BGE-base re-predicting 256
+in-flight requests (trace-shaped prompt+partial-response lengths, synthetic
+tokens, random-init weights) + ISRTF select with batch_cap 4 (the paper's batch-4
+evaluation).  With --gpus N (torchrun, NCCL) every rank re-predicts its own
+256 requests (weak scaling) and the batch is selected over all N x 256 requests by
+elis_isrtf_select_dist (local top-cap -> NCCL all-gather -> identical merge).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl elis|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2505_09142_b200 import inputs  # noqa: E402
+
+METRIC = "ISRTF re-predict+select predictions/sec and ms/iteration at 1/2/4/8 B200"
+UNIT = "predictions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["elis", "reference"], default="elis")
+    ap.add_argument("--config", choices=["tiny", "base", "large"], default="base")
+    ap.add_argument("--n", type=int, default=256, help="requests re-predicted per GPU per step")
+    ap.add_argument("--lengths", default="trace", help="trace | uniform | fixed:L")
+    ap.add_argument("--cap", type=int, default=4, help="batch_cap")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=12, help="requests in the oracle sample")
+    return ap.parse_args()
+
+
+def workload(args, rank: int):
+    n = args.n
+    seed = args.seed * 1000 + rank
+    if args.lengths == "trace":
+        L, gen, _ = inputs.trace_lengths(n, seed=seed)
+    elif args.lengths == "uniform":
+        L = inputs.uniform_lengths(n, seed=seed)
+        gen = np.zeros(n, np.int32)
+    elif args.lengths.startswith("fixed:"):
+        L = np.full(n, int(args.lengths.split(":")[1]), np.int32)
+        gen = np.zeros(n, np.int32)
+    else:
+        raise SystemExit(f"unknown --lengths {args.lengths}")
+    tokens = inputs.make_tokens(L, seed=seed)
+    return L.astype(np.int32), gen.astype(np.int32), tokens
+
+
+def config_desc(args, T_local, world):
+    return {
+        "workload": (f"cfg{ {'tiny': 1, 'base': 2, 'large': 3}[args.config] }: {args.config} encoder re-predicting "
+                     f"{args.n} in-flight requests per GPU ({args.lengths} lengths) + ISRTF select batch_cap "
+                     f"{args.cap}" + (f" over {world}x{args.n} via NCCL all-gather" if world > 1 else "")),
+        "encoder": args.config,
+        "requests_per_gpu": args.n,
+        "tokens_per_gpu_step": int(T_local),
+        "lengths": args.lengths,
+        "batch_cap": args.cap,
+        "pooling": "mean",
+        "parallelism": f"request-sharded dp{world}" if world > 1 else "single GPU",
+        "l2": "no flush: per-step working set (218 MB bf16 weights + >=0.5 GB activations) exceeds the 126 MB L2",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                      "-i", str(self.idx)], capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(k)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- roofline
+def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic_table: dict):
+    """Dominant kernel class (largest share of device time) -> achieved vs measured peak."""
+    H, F, nl = cfg.hidden, cfg.intermediate, cfg.num_layers
+    flops = {  # algorithmic FLOPs per launch
+        "gemm_qkv": 2.0 * T * H * 3 * H,
+        "gemm_out": 2.0 * T * H * H,
+        "gemm_ffn1": 2.0 * T * H * F,
+        "gemm_ffn2": 2.0 * T * F * H,
+        "attention": 4.0 * H * float(np.sum(L.astype(np.float64) ** 2)),
+    }
+    bytes_ = {  # algorithmic HBM bytes per launch
+        "layernorm": 10.0 * T * H,          # read u f32, write h f32 + h bf16
+        "embed_ln": T * (4 + 2 * H + 10.0 * H),
+    }
+    name, (ms, cnt) = max(prof.items(), key=lambda kv: kv[1][0])
+    avg_s = ms / cnt / 1e3
+    if name in flops:
+        bound, unit = "tensor", "TFLOP/s"
+        achieved = flops[name] / avg_s / 1e12
+        peak = peaks.get("bf16_tflops_sustained") or 1400.0
+        peak_src = "measured sustained bf16 (MEASURED_PEAKS.json)" if peaks.get("bf16_tflops_sustained") else "fallback"
+    else:
+        bound, unit = "hbm", "GB/s"
+        achieved = bytes_.get(name, 0.0) / avg_s / 1e9
+        peak = peaks.get("hbm_gbs") or 6650.0
+        peak_src = "measured copy (MEASURED_PEAKS.json)" if peaks.get("hbm_gbs") else "fallback"
+    tr = traffic_table.get(name)
+    total = sum(v[0] for v in prof.values())
+    return {"kernel": name, "bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": tr, "peak_source": peak_src,
+            "avg_launch_us": round(avg_s * 1e6, 2), "share_of_step": round(ms / total, 4)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def cpu_sample_idx(L: np.ndarray, k: int):
+    order = np.argsort(L, kind="stable")
+    return sorted(set(order[np.linspace(0, len(L) - 1, k).astype(int)].tolist()))
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads") or 1) for i in threadpool_info()) or os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def time_oracle(cfg, W, L, gen, tokens, idx, cap):
+    from oracle import head as ohead
+    from oracle.select import isrtf_select
+    t0 = time.perf_counter()
+    pred = ohead.predict(tokens, L, W, cfg, requests=idx)
+    isrtf_select(pred.astype(np.float32), gen[idx], cap)
+    return time.perf_counter() - t0, int(np.sum(L[idx]))
+
+
+# ----------------------------------------------------------------------------- main arms
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """Reference arm = the fp64 oracle (this tier has no reference implementation), timed on
+    the host cores on a bounded sample of the same workload per step."""
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    cfg = inputs.CONFIGS[args.config]
+    W = inputs.make_weights(cfg, seed=0)
+    L, gen, tokens = workload(args, 0)
+    per_step = 2
+    pool = cpu_sample_idx(L, max(per_step * (args.steps + args.warmup), per_step))
+    secs, reqs, toks = [], 0, 0
+    for s in range(args.warmup + args.steps):
+        idx = pool[(s * per_step) % len(pool):(s * per_step) % len(pool) + per_step] or pool[:per_step]
+        dt, nt = time_oracle(cfg, W, L, gen, tokens, idx, args.cap)
+        if s >= args.warmup:
+            secs.append(dt)
+            reqs += len(idx)
+            toks += nt
+    total = sum(secs)
+    value = reqs / total
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_desc(args, int(L.sum()), 1),
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+                            "sample": f"{per_step} length-stratified requests of the workload per step "
+                                      f"(+ oracle select over them); {toks} tokens total"},
+           "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "tokens_per_s": round(toks / total, 2)}
+    print(json.dumps(out), flush=True)
+
+
+def run_elis(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_09142_b200 import binding
+
+    world, rank, local = dist_env()
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = inputs.CONFIGS[args.config]
+    W = inputs.make_weights(cfg, seed=0)
+    L, gen, tokens = workload(args, rank)
+    n, T = len(L), int(L.sum())
+    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local)
+    if world > 1:
+        uid = binding.nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        P.dist_attach(rank, world, obj[0])
+
+    st = torch.cuda.current_stream()
+    d_tok = torch.from_numpy(tokens).cuda()
+    d_len = torch.from_numpy(L).cuda()
+    d_gen = torch.from_numpy(gen).cuda()
+    d_pred = torch.empty(n, device="cuda")
+    d_ids = torch.empty(args.cap, dtype=torch.int32, device="cuda")
+    d_cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+
+    def step():
+        P.predict_remaining(d_tok, d_len, T, d_pred, stream=st)
+        if world > 1:
+            P.isrtf_select_dist(d_pred, d_gen, rank * n, args.cap, d_ids, out_count=d_cnt, stream=st)
+        else:
+            P.isrtf_select(d_pred, d_gen, args.cap, d_ids, out_count=d_cnt, stream=st)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    if P.sync_status() != 0:
+        raise SystemExit("device error during warm-up: " + binding.lib().elis_last_error().decode())
+
+    # ---------------- timed region (device events on the launching stream)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    sampler = ClockSampler(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.launch_count()
+    P.profile_enable(True)
+    if sampler:
+        sampler.__enter__()
+    ev[0].record(st)
+    for k in range(args.steps):
+        step()
+        ev[k + 1].record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    if sampler:
+        sampler.__exit__()
+    launches = P.launch_count() - launches0
+    prof = P.profile_read()
+    P.profile_enable(False)
+    per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = world * n * args.steps / (total_ms / 1e3)
+
+    # ---------------- end to end through the public C ABI with host buffers
+    h_tok = torch.from_numpy(tokens).pin_memory()
+    h_len = torch.from_numpy(L).pin_memory()
+    h_gen = torch.from_numpy(gen).pin_memory()
+    h_ids = torch.empty(args.cap, dtype=torch.int32).pin_memory()
+    h_cnt = torch.empty(1, dtype=torch.int32).pin_memory()
+    goff = rank * n if world > 1 else -1
+    for _ in range(2):
+        P.iteration_host(h_tok, h_len, h_gen, args.cap, h_ids, h_cnt, global_offset=goff, stream=st)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        P.iteration_host(h_tok, h_len, h_gen, args.cap, h_ids, h_cnt, global_offset=goff, stream=st)
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * n * args.steps / float(e2e_s.item())
+
+    out = None
+    if rank == 0:
+        peaks = load_peaks()
+        roof = kernel_roofline(prof, cfg, T, L, peaks, load_traffic())
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "ms_per_step_p10_p50_p90": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90)],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded trace-shaped lengths, uniform token ids, random-init BGE weights)",
+            "config": config_desc(args, T, world),
+            "tokens_per_s": round(world * T * args.steps / (total_ms / 1e3), 1),
+            "roofline": roof,
+            "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items())},
+            "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(4 * T + 4 * n + 4 * n), "d2h_bytes_per_step": int(4 * args.cap + 4)},
+            "gpu_launches": int(launches),
+            "clocks": sampler.summary() if sampler else None,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            idx = cpu_sample_idx(L, args.cpu_sample)
+            dt, nt = time_oracle(cfg, W, L, gen, tokens, idx, args.cap)
+            out["cpu_baseline"] = {"value": round(len(idx) / dt, 4), "unit": UNIT, "cores": oracle_threads(),
+                                   "kind": "oracle",
+                                   "sample": f"{len(idx)} length-stratified requests of this workload ({nt} tokens) "
+                                             f"encoded + selected by the fp64 numpy oracle"}
+    P.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_elis(args)
+
+
+if __name__ == "__main__":
+    main()

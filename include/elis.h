@@ -161,12 +161,14 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
  * One scheduling iteration from host memory: H2D copy of tokens/lengths/generated
  * (+ order/running if given), predict, select, D2H copy of out_ids/out_count (and
  * out_pred if non-NULL).  Synchronises `stream` before returning.  Pinned host memory
- * gives asynchronous copies. */
+ * gives asynchronous copies.  global_offset < 0: single-GPU elis_isrtf_select;
+ * global_offset >= 0: elis_isrtf_select_dist over the attached communicator (this
+ * rank's slots start at global_offset; out_ids are global). */
 elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, const int32_t* h_lengths,
                                 int32_t n, int64_t total_tokens, const int32_t* h_generated,
                                 const uint32_t* h_order, const uint8_t* h_running, int32_t policy,
-                                int32_t allow_preempt, int32_t batch_cap, int32_t* h_out_ids,
-                                int32_t* h_out_count, float* h_out_pred, void* stream);
+                                int32_t allow_preempt, int32_t batch_cap, int32_t global_offset,
+                                int32_t* h_out_ids, int32_t* h_out_count, float* h_out_pred, void* stream);
 
 /* Synchronise the stream of the last call and return (and clear) the sticky device
  * error word: ELIS_ERR_DEVICE_INPUT if set, else ELIS_OK / ELIS_ERR_CUDA. */

@@ -64,8 +64,8 @@ def lib():
         "elis_nccl_unique_id": (_i32, [_vp]),
         "elis_dist_attach": (_i32, [_vp, _i32, _i32, _vp]),
         "elis_isrtf_select_dist": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
-        "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
-                                       _vp, _vp]),
+        "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp,
+                                       _vp, _vp, _vp]),
         "elis_sync_status": (_i32, [_vp]),
         "elis_last_device_error_bits": (_u32, [_vp]),
         "elis_status_string": (ctypes.c_char_p, [_i32]),
@@ -175,11 +175,13 @@ class Predictor:
     def iteration_host(self, tokens: np.ndarray, lengths: np.ndarray, generated: np.ndarray, batch_cap: int,
                        out_ids: np.ndarray, out_count: np.ndarray | None = None, out_pred: np.ndarray | None = None,
                        order: np.ndarray | None = None, running: np.ndarray | None = None, policy=POLICY_ISRTF,
-                       allow_preempt=True, stream=None):
-        """Host buffers in (numpy or pinned torch CPU tensors), ids out; synchronises."""
+                       allow_preempt=True, global_offset: int = -1, stream=None):
+        """Host buffers in (numpy or pinned torch CPU tensors), ids out; synchronises.
+        global_offset >= 0 selects globally over the attached NCCL communicator."""
         check(lib().elis_iteration_host(self.h, _ptr(tokens), _ptr(lengths), int(lengths.shape[0]),
                                         int(tokens.shape[0]), _ptr(generated), _ptr(order), _ptr(running),
-                                        int(policy), int(allow_preempt), int(batch_cap), _ptr(out_ids),
+                                        int(policy), int(allow_preempt), int(batch_cap), int(global_offset),
+                                        _ptr(out_ids),
                                         _ptr(out_count), _ptr(out_pred), _stream(stream)), "elis_iteration_host")
 
     # ---- instrumentation

@@ -568,7 +568,8 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
 elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, const int32_t* h_lengths, int32_t n,
                                 int64_t total_tokens, const int32_t* h_generated, const uint32_t* h_order,
                                 const uint8_t* h_running, int32_t policy, int32_t allow_preempt, int32_t batch_cap,
-                                int32_t* h_out_ids, int32_t* h_out_count, float* h_out_pred, void* stream) {
+                                int32_t global_offset, int32_t* h_out_ids, int32_t* h_out_count, float* h_out_pred,
+                                void* stream) {
   if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
   if (n < 1 || n > p->cfg.max_requests) return fail(ELIS_ERR_INVALID_ARG, "n outside [1, max_requests]");
   if (!h_tokens || !h_lengths || !h_generated || !h_out_ids) return fail(ELIS_ERR_INVALID_ARG, "NULL host array");
@@ -596,7 +597,10 @@ elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, cons
   pre.order = h_order ? p->d_order : nullptr;
   pre.running = h_running ? p->d_running : nullptr;
   pre.out_count = p->d_count;
-  s = elis_isrtf_select(p, p->d_pred, p->d_generated, n, batch_cap, &pre, p->d_ids, stream);
+  if (global_offset >= 0)
+    s = elis_isrtf_select_dist(p, p->d_pred, p->d_generated, n, global_offset, batch_cap, &pre, p->d_ids, stream);
+  else
+    s = elis_isrtf_select(p, p->d_pred, p->d_generated, n, batch_cap, &pre, p->d_ids, stream);
   if (s != ELIS_OK) return s;
   CUDA_TRY(cudaMemcpyAsync(h_out_ids, p->d_ids, static_cast<size_t>(batch_cap) * 4, cudaMemcpyDeviceToHost, st));
   if (h_out_count) CUDA_TRY(cudaMemcpyAsync(h_out_count, p->d_count, 4, cudaMemcpyDeviceToHost, st));

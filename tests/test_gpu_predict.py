@@ -15,6 +15,7 @@ torch = pytest.importorskip("torch")
 
 PRED_RTOL = 1e-2
 HIDDEN_ATOL = 2e-2
+CLS_PRED_RTOL = 3e-2
 
 
 def make_predictor(name, max_tokens, max_requests, pooling=inputs.POOL_MEAN, **kw):
@@ -59,8 +60,10 @@ def test_cfg1_tiny_full_parity_and_select(cuda_lib, pooling):
     if pooling == inputs.POOL_MEAN:
         assert rel_err(gpu, ref).max() <= PRED_RTOL, rel_err(gpu, ref).max()
     else:
-        # CLS pooling: report error relative to the prediction spread
-        assert (np.abs(gpu - ref) / ref.std()).max() <= 5e-2
+        # CLS pooling (P:138 reading): one row feeds the head, nothing averages the bf16
+        # operand error, and the calibrated head gain amplifies it -- DESIGN.md "Tolerances"
+        # states the looser measured bound used for this non-default reading.
+        assert rel_err(gpu, ref).max() <= CLS_PRED_RTOL, rel_err(gpu, ref).max()
     # selection: bit-exact vs the oracle on the GPU's own fp32 predictions
     gen = np.zeros(16, np.int32)
     running = np.zeros(16, np.uint8)
