@@ -26,6 +26,13 @@ typedef enum {
 elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias, const float* residual,
                          void* out, int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream);
 
+/* tcgen05 GEMM with the fused residual + LayerNorm epilogue (attention-output / FFN2 of a
+ * post-LN BERT block): v = A W^T + bias + resid_inout; resid_inout <- LN(v; gamma, beta, eps)
+ * (fp32, in place) and outb <- bf16(LN(v)).  N / (N % 256 ? 128 : 256) <= 4 (one cluster per row). */
+elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* bias, float* resid_inout,
+                            const float* gamma, const float* beta, float eps, uint16_t* outb, int32_t M, int32_t N,
+                            int32_t K, void* stream);
+
 /* Varlen bidirectional multi-head attention ("process tokens in parallel").
  * qkv bf16 [T, 3H] (Q | K | V, head h at columns h*d .. h*d+d-1 of each third),
  * lengths int32 [n] (sum == T, each in [1, 512]); ctx bf16 [T, H] = per request i and head h:

@@ -75,6 +75,7 @@ def lib():
         "elis_profile_enable": (_i32, [_vp, _i32]),
         "elis_profile_read": (_i32, [_vp, _vp, _vp, _vp, _i32]),
         "elis_op_gemm": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+        "elis_op_gemm_ln": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _i32, _i32, _i32, _vp]),
         "elis_op_attention": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
         "elis_op_layernorm": (_i32, [_vp, _vp, _vp, _f32, _i64, _i32, _vp, _vp, _vp]),
         "elis_op_fc_f32": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
@@ -221,6 +222,13 @@ def op_gemm(A, W, bias, out, epilogue: int, residual=None, stream=None):
     N = W.shape[0]
     check(lib().elis_op_gemm(_ptr(A), _ptr(W), _ptr(bias), _ptr(residual), _ptr(out), M, N, K, epilogue,
                              _stream(stream)), "elis_op_gemm")
+
+
+def op_gemm_ln(A, W, bias, resid_inout, gamma, beta, eps: float, outb, stream=None):
+    M, K = A.shape
+    N = W.shape[0]
+    check(lib().elis_op_gemm_ln(_ptr(A), _ptr(W), _ptr(bias), _ptr(resid_inout), _ptr(gamma), _ptr(beta), eps,
+                                _ptr(outb), M, N, K, _stream(stream)), "elis_op_gemm_ln")
 
 
 def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None):

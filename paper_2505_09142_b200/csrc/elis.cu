@@ -137,7 +137,7 @@ struct elis_predictor {
   std::vector<int> head_dims;
 
   // workspaces
-  float *h32 = nullptr, *u32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
+  float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
   uint16_t *hb = nullptr, *qkv = nullptr, *ctx = nullptr, *g = nullptr;
   int32_t* cu = nullptr;
   int2* work = nullptr;
@@ -368,7 +368,6 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
 
   // ---- workspaces
   ALLOC(p->h32, static_cast<size_t>(T) * H);
-  ALLOC(p->u32, static_cast<size_t>(T) * H);
   ALLOC(p->hb, static_cast<size_t>(T) * H);
   ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
   ALLOC(p->ctx, static_cast<size_t>(T) * H);
@@ -395,11 +394,18 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   // ---- GEMM plans (TMA descriptors over the fixed workspaces; M set per call)
   for (int l = 0; l < cfg->num_layers; ++l) {
     Layer& L = p->layers[l];
+    // out-proj and FFN2 carry the residual add + LayerNorm in their epilogue (in place on h32)
     bool ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
-              make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->u32, 0, H, H, EPI_BIAS_RESID_F32) &&
+              make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
               make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
-              make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->u32, 0, H, F, EPI_BIAS_RESID_F32);
+              make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    L.p_out.args.outb = L.p_ffn2.args.outb = p->hb;
+    L.p_out.args.gamma = L.ln1g;
+    L.p_out.args.beta = L.ln1b;
+    L.p_ffn2.args.gamma = L.ln2g;
+    L.p_ffn2.args.beta = L.ln2b;
+    L.p_out.args.eps = L.p_ffn2.args.eps = cfg->ln_eps;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "create sync");
 #undef ALLOC
@@ -430,14 +436,12 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   const int64_t tiles = attn_max_tiles(total_tokens, n);
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
-    L.p_qkv.M = L.p_out.M = L.p_ffn1.M = L.p_ffn2.M = M;
+    L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     LAUNCH(p, PC_ATTN, st, launch_attention(p->qkv, p->cu, p->work, p->num_work, tiles, H, c.num_heads, p->ctx, st));
-    LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));
-    LAUNCH(p, PC_LN, st, launch_layernorm(p->u32, L.ln1g, L.ln1b, c.ln_eps, total_tokens, H, p->h32, p->hb, st));
-    LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));
-    LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));
-    LAUNCH(p, PC_LN, st, launch_layernorm(p->u32, L.ln2g, L.ln2b, c.ln_eps, total_tokens, H, p->h32, p->hb, st));
+    LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
+    LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
+    LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
   }
   LAUNCH(p, PC_POOL, st, launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
   const float* x = p->pooled;
@@ -676,6 +680,26 @@ elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias
   GemmPlan g;
   if (!make_gemm_plan(&g, A, M, W, bias, residual, out, M, N, K, epilogue))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* bias, float* resid_inout,
+                            const float* gamma, const float* beta, float eps, uint16_t* outb, int32_t M, int32_t N,
+                            int32_t K, void* stream) {
+  if (!A || !W || !bias || !resid_inout || !gamma || !beta || !outb || M < 1 || N < 128 || N % 128 || K < 64 ||
+      K % 64 || N / gemm_block_n(N) > 4)
+    return fail(ELIS_ERR_INVALID_ARG, "gemm_ln arguments");
+  GemmPlan g;
+  if (!make_gemm_plan(&g, A, M, W, bias, resid_inout, resid_inout, M, N, K, EPI_BIAS_RESID_LN))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  g.args.outb = outb;
+  g.args.gamma = gamma;
+  g.args.beta = beta;
+  g.args.eps = eps;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

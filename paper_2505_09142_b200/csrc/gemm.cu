@@ -1,22 +1,29 @@
 // gemm.cu -- dense encoder GEMMs on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-//   C[M, N] = A[M, K] * W[N, K]^T + bias  (+ GELU | + fp32 residual)
+//   C[M, N] = A[M, K] * W[N, K]^T + bias  (+ GELU | + fp32 residual | + residual -> LayerNorm)
 //
-// The QKV, attention-output and FFN contractions of every BERT block
-// (BGE = BERT-base).  Both operands
-// are K-major (activations row-major, nn.Linear weights [out, in]) which is the
-// natural tcgen05 layout.
+// The QKV, attention-output and FFN contractions of every BERT block (SURVEY.md Sec. 8a
+// rows a3/a5/a7/a8; BGE = BERT-base).  Both operands are K-major (activations
+// row-major, nn.Linear weights [out, in]), the natural tcgen05 layout.
 //
 // Design (sm_100a):
-//   * persistent grid (<= one CTA per SM), static round-robin tile schedule;
-//   * warp 0 = TMA producer (SWIZZLE_128B 128x64 / BNx64 bf16 slabs, mbarrier ring),
-//     warp 1 = single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per instruction),
-//     warp 2 = TMEM allocator, warps 4..7 = epilogue (tcgen05.ld -> bias/GELU/residual
-//     -> global);
-//   * two TMEM accumulators (2 x BN columns) so the epilogue of tile i overlaps the
-//     mainloop of tile i+1;
+//   * persistent grid, static tile schedule; warp 0 = TMA producer (SWIZZLE_128B slabs,
+//     mbarrier ring), warp 1 = single-thread tcgen05.mma issuer (M=128, N=BN, K=16),
+//     warp 2 = TMEM allocator, warps 4..11 = epilogue (two warps per TMEM lane quarter,
+//     each owning half of the tile's columns);
+//   * two TMEM accumulators (2 x BN columns): the epilogue of tile i overlaps the mainloop
+//     of tile i+1;
 //   * ragged M handled by TMA out-of-bounds zero fill + masked stores (no padding of T);
 //   * no split-K: every output row depends on its own A row only (batch invariance).
+//
+// EPI_BIAS_RESID_LN (attention-output and FFN2 + LayerNorm, rows a5+a6 / a8): a row of
+// H = 768 / 1024 columns spans CS = H / 256 CTAs, launched as one thread-block cluster.
+// Each CTA adds bias + fp32 residual, keeps v in TMEM (tcgen05.st), computes per-row
+// (mean, M2) over its columns and pushes them into every peer's shared memory over DSMEM
+// (st.shared::cluster + remote mbarrier arrive); after the exchange every CTA merges the
+// CS partials in rank order (Chan) and normalises its columns.  The fp32 residual stream
+// is updated in place and the bf16 copy for the next GEMM is written in the same pass:
+// 10 B/element of epilogue traffic instead of 18 B with a separate LayerNorm kernel.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -26,7 +33,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kGemmThreads = 256;
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 128 + kEpiWarps * 32;  // 4 control warps + 8 epilogue warps
+constexpr int kMaxCluster = 4;
 
 template <int BN>
 struct GemmCfg {
@@ -35,34 +44,58 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int CHUNKS_PER_WARP = BN / 64;  // 32-column chunks per epilogue warp
+  // barriers + LN scratch: stats[2 slots][kMaxCluster][128] float2 + part[2][128] float2
+  static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + AUX_BYTES;
 };
 
 ELIS_DEV float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f)); }
 
+// Chan et al. merge of (count, mean, M2) partial statistics.
+ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
+  const float n = n_a + n_b;
+  const float d = mean_b - mean_a;
+  mean_a = mean_a + d * (n_b / n);
+  m2_a = m2_a + m2_b + d * d * (n_a * n_b / n);
+  n_a = n;
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const float* __restrict__ bias, const float* __restrict__ resid, void* __restrict__ out, int M,
-              int N, int K) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
   using C = GemmCfg<BN>;
+  constexpr bool LN = (EPI == EPI_BIAS_RESID_LN);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* aux = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;  // LN: stats slots filled by every CTA of the cluster
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + 2);
+  float2* stats = reinterpret_cast<float2*>(aux + 512);         // [2][kMaxCluster][128]
+  float2* part = stats + 2 * kMaxCluster * 128;                  // [2 halves][128]
 
   const int warp = warp_id();
   const int lane = lane_id();
+  const int M = args.M, N = args.N, K = args.K;
   const int num_m = (M + BM - 1) / BM;
   const int num_n = N / BN;
-  const int num_tiles = num_m * num_n;
   const int num_k = K / BK;
+  // Tile schedule.  LN: cluster c owns M-tiles c, c + ncl, ...; CTA rank r owns N-tile r.
+  const int cs = LN ? num_n : 1;
+  const int rank = LN ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cid = LN ? static_cast<int>(blockIdx.x) / cs : static_cast<int>(blockIdx.x);
+  const int ncl = LN ? static_cast<int>(gridDim.x) / cs : static_cast<int>(gridDim.x);
+  const int num_iter_tiles = LN ? num_m : num_m * num_n;
+  auto tile_mn = [&](int t, int& m, int& n) {
+    if (LN) { m = t; n = rank; } else { m = t / num_n; n = t % num_n; }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -73,13 +106,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiWarps * 32);
+      mbar_init(&sfull[a], 128 * cs);
     }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (LN) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -88,8 +122,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m = tile / num_n, n = tile % num_n;
+      for (int t = cid; t < num_iter_tiles; t += ncl) {
+        int m, n;
+        tile_mn(t, m, n);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1u);
           mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
@@ -106,7 +141,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1u);
@@ -130,52 +165,135 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global
-    const int q = warp - 4;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;    // which half of the tile's columns
+    const int row_in_tile = q * 32 + lane;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int m = tile / num_n, n = tile % num_n;
+    for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
+      int m, n;
+      tile_mn(t, m, n);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row = m * BM + q * 32 + lane;
+      const int row = m * BM + row_in_tile;
+      const bool row_ok = row < M;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      const int cbase = half * (BN / 2);  // first tile column of this warp
+      float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // LN row statistics over this warp's columns
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < C::CHUNKS_PER_WARP; ++c) {
+        const int tcol = cbase + c * 32;
+        const int col0 = n * BN + tcol;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_32x32b_x32(taddr + tcol, r);
         tc_wait_ld();
-        const int col0 = n * BN + c * 32;
-        if (row < M) {
-          float v[32];
-          const float4* b4 = reinterpret_cast<const float4*>(bias + col0);
+        float v[32];
+        const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 bb = __ldg(b4 + j);
-            v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bb.x;
-            v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
-            v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
-            v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
-          }
-          if constexpr (EPI == EPI_BIAS_RESID_F32) {
-            const float4* r4 = reinterpret_cast<const float4*>(resid + static_cast<size_t>(row) * N + col0);
-            float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(out) + static_cast<size_t>(row) * N + col0);
+        for (int j = 0; j < 8; ++j) {
+          const float4 bb = __ldg(b4 + j);
+          v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bb.x;
+          v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
+          v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
+          v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
+        }
+        if constexpr (EPI == EPI_BIAS_RESID_F32 || LN) {
+          if (row_ok) {
+            const float4* r4 = reinterpret_cast<const float4*>(args.resid + static_cast<size_t>(row) * N + col0);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 rr = __ldg(r4 + j);
-              o4[j] = make_float4(v[4 * j] + rr.x, v[4 * j + 1] + rr.y, v[4 * j + 2] + rr.z, v[4 * j + 3] + rr.w);
+              v[4 * j] += rr.x; v[4 * j + 1] += rr.y; v[4 * j + 2] += rr.z; v[4 * j + 3] += rr.w;
             }
+          }
+        }
+        if constexpr (LN) {
+          // chunk statistics, merged into the running (n, mean, M2); v kept in TMEM
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) s += v[j];
+          const float cm = s * (1.0f / 32.0f);
+          float m2 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) { const float d = v[j] - cm; m2 = fmaf(d, d, m2); }
+          if (c == 0) { st_n = 32.f; st_mean = cm; st_m2 = m2; }
+          else chan_merge(st_n, st_mean, st_m2, 32.f, cm, m2);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+          tmem_st_32x32b_x32(taddr + tcol, r);
+        } else if (row_ok) {
+          if constexpr (EPI == EPI_BIAS_RESID_F32) {
+            float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
             if constexpr (EPI == EPI_BIAS_GELU_BF16) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
             }
-            uint4* o4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + static_cast<size_t>(row) * N + col0);
+            uint4* o4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + static_cast<size_t>(row) * N + col0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 4; ++j)
               o4[j] = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
                                  pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+          }
+        }
+      }
+      if constexpr (LN) {
+        tc_wait_st();
+        const int slot = it & 1;
+        const uint32_t sph = (it >> 1) & 1;
+        part[half * 128 + row_in_tile] = make_float2(st_mean, st_m2);
+        named_bar_sync(1, kEpiWarps * 32);
+        if (half == 0) {
+          // this CTA's statistics over its BN columns -> every CTA of the cluster
+          float cn = st_n, cmean = st_mean, cm2 = st_m2;
+          const float2 o = part[128 + row_in_tile];
+          chan_merge(cn, cmean, cm2, st_n, o.x, o.y);
+          const uint32_t lslot = smem_u32(&stats[(slot * kMaxCluster + rank) * 128 + row_in_tile]);
+          const uint32_t lbar = smem_u32(&sfull[slot]);
+          for (int peer = 0; peer < cs; ++peer) {
+            st_cluster_f32x2(mapa_shared(lslot, peer), cmean, cm2);
+            mbar_arrive_remote_release(mapa_shared(lbar, peer));
+          }
+        }
+        mbar_wait_acquire_cluster(&sfull[slot], sph);
+        // merge the cs partials in rank order (identical on every CTA) -> mean, rstd
+        float tn = 0.f, tmean = 0.f, tm2 = 0.f;
+        for (int p = 0; p < cs; ++p) {
+          const float2 s2 = stats[(slot * kMaxCluster + p) * 128 + row_in_tile];
+          if (p == 0) { tn = static_cast<float>(BN); tmean = s2.x; tm2 = s2.y; }
+          else chan_merge(tn, tmean, tm2, static_cast<float>(BN), s2.x, s2.y);
+        }
+        const float rstd = 1.0f / sqrtf(tm2 / tn + args.eps);
+#pragma unroll 1
+        for (int c = 0; c < C::CHUNKS_PER_WARP; ++c) {
+          const int tcol = cbase + c * 32;
+          const int col0 = n * BN + tcol;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + tcol, r);
+          tc_wait_ld();
+          if (row_ok) {
+            float y[32];
+            const float4* g4 = reinterpret_cast<const float4*>(args.gamma + col0);
+            const float4* be4 = reinterpret_cast<const float4*>(args.beta + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 g = __ldg(g4 + j), be = __ldg(be4 + j);
+              y[4 * j + 0] = (__uint_as_float(r[4 * j + 0]) - tmean) * rstd * g.x + be.x;
+              y[4 * j + 1] = (__uint_as_float(r[4 * j + 1]) - tmean) * rstd * g.y + be.y;
+              y[4 * j + 2] = (__uint_as_float(r[4 * j + 2]) - tmean) * rstd * g.z + be.z;
+              y[4 * j + 3] = (__uint_as_float(r[4 * j + 3]) - tmean) * rstd * g.w + be.w;
             }
+            float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o4[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+            uint4* ob = reinterpret_cast<uint4*>(args.outb + static_cast<size_t>(row) * N + col0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              ob[j] = make_uint4(pack_bf16x2(y[8 * j + 0], y[8 * j + 1]), pack_bf16x2(y[8 * j + 2], y[8 * j + 3]),
+                                 pack_bf16x2(y[8 * j + 4], y[8 * j + 5]), pack_bf16x2(y[8 * j + 6], y[8 * j + 7]));
           }
         }
       }
@@ -183,7 +301,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_arrive(&tempty[acc]);
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if (LN) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -193,17 +312,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 template <int BN, int EPI>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   using C = GemmCfg<BN>;
-  static bool attr_set = false;  // per (BN, EPI) instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  auto kern = k_gemm_tc<BN, EPI>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int num_m = (g.args.M + BM - 1) / BM;
+  const int num_n = g.args.N / BN;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (EPI == EPI_BIAS_RESID_LN) {
+    const int cs = num_n;
+    if (cs > kMaxCluster) return cudaErrorInvalidValue;
+    if (cs > 1) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    // number of clusters that can be co-resident (one CTA per SM, cluster of cs)
+    static int max_clusters[kMaxCluster + 1] = {0, 0, 0, 0, 0};
+    if (max_clusters[cs] == 0) {
+      cudaLaunchConfig_t q = cfg;
+      q.gridDim = dim3(cs * (num_sms / cs));
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      q.attrs = attr;
+      q.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc <= 0) mc = num_sms / cs;
+      max_clusters[cs] = mc;
+    }
+    const int ncl = num_m < max_clusters[cs] ? num_m : max_clusters[cs];
+    cfg.gridDim = dim3(cs * ncl);
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  } else {
+    const int tiles = num_m * num_n;
+    cfg.gridDim = dim3(tiles < num_sms ? tiles : num_sms);
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
   }
-  const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  k_gemm_tc<BN, EPI><<<grid, kGemmThreads, C::SMEM_BYTES, st>>>(g.tmA, g.tmB, g.bias, g.resid, g.out, g.M, g.N,
-                                                                  g.K);
+  e = cudaLaunchKernelEx(&cfg, kern, g.tmA, g.tmB, g.args);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -212,15 +368,17 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
 int gemm_block_n(int N) { return (N % 256 == 0) ? 256 : 128; }
 
 cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
-  if (g.M <= 0) return cudaSuccess;
-  const int bn = gemm_block_n(g.N);
-  switch (g.epi * 2 + (bn == 256 ? 1 : 0)) {
-    case EPI_BIAS_BF16 * 2 + 0: return launch_bn<128, EPI_BIAS_BF16>(g, num_sms, st);
-    case EPI_BIAS_BF16 * 2 + 1: return launch_bn<256, EPI_BIAS_BF16>(g, num_sms, st);
-    case EPI_BIAS_GELU_BF16 * 2 + 0: return launch_bn<128, EPI_BIAS_GELU_BF16>(g, num_sms, st);
-    case EPI_BIAS_GELU_BF16 * 2 + 1: return launch_bn<256, EPI_BIAS_GELU_BF16>(g, num_sms, st);
-    case EPI_BIAS_RESID_F32 * 2 + 0: return launch_bn<128, EPI_BIAS_RESID_F32>(g, num_sms, st);
-    case EPI_BIAS_RESID_F32 * 2 + 1: return launch_bn<256, EPI_BIAS_RESID_F32>(g, num_sms, st);
+  if (g.args.M <= 0) return cudaSuccess;
+  const int bn = gemm_block_n(g.args.N);
+  const bool b256 = bn == 256;
+  switch (g.epi) {
+    case EPI_BIAS_BF16: return b256 ? launch_bn<256, EPI_BIAS_BF16>(g, num_sms, st) : launch_bn<128, EPI_BIAS_BF16>(g, num_sms, st);
+    case EPI_BIAS_GELU_BF16:
+      return b256 ? launch_bn<256, EPI_BIAS_GELU_BF16>(g, num_sms, st) : launch_bn<128, EPI_BIAS_GELU_BF16>(g, num_sms, st);
+    case EPI_BIAS_RESID_F32:
+      return b256 ? launch_bn<256, EPI_BIAS_RESID_F32>(g, num_sms, st) : launch_bn<128, EPI_BIAS_RESID_F32>(g, num_sms, st);
+    case EPI_BIAS_RESID_LN:
+      return b256 ? launch_bn<256, EPI_BIAS_RESID_LN>(g, num_sms, st) : launch_bn<128, EPI_BIAS_RESID_LN>(g, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -259,13 +417,15 @@ bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint6
 bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
                     const float* resid, void* out, int M, int N, int K, int epi) {
   if (N % 128 != 0 || K % BK != 0 || M < 0) return false;
-  g->M = M;
-  g->N = N;
-  g->K = K;
+  if (epi == EPI_BIAS_RESID_LN && N / gemm_block_n(N) > kMaxCluster) return false;
   g->epi = epi;
-  g->bias = bias;
-  g->resid = resid;
-  g->out = out;
+  g->args = GemmArgs{};
+  g->args.M = M;
+  g->args.N = N;
+  g->args.K = K;
+  g->args.bias = bias;
+  g->args.resid = resid;
+  g->args.out = out;
   if (!make_tmap_bf16_kmajor(&g->tmA, A, a_rows, K, BM)) return false;
   if (!make_tmap_bf16_kmajor(&g->tmB, W, N, K, gemm_block_n(N))) return false;
   return true;

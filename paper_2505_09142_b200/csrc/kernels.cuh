@@ -7,19 +7,27 @@
 
 namespace elis {
 
-enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2 };
+enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BIAS_RESID_LN = 3 };
 
 // Device error bits (sticky; see elis.h).
 enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u };
 
 // ---- GEMM (gemm.cu)
+struct GemmArgs {
+  const float* bias;
+  const float* resid;   // f32 [M, N] (RESID_F32, RESID_LN; may alias out for RESID_LN)
+  void* out;            // bf16 or f32 [M, N]
+  uint16_t* outb;       // RESID_LN: bf16 copy of the normalised rows
+  const float* gamma;   // RESID_LN
+  const float* beta;    // RESID_LN
+  float eps;
+  int M, N, K;
+};
 struct GemmPlan {
   CUtensorMap tmA;
   CUtensorMap tmB;
-  const float* bias;
-  const float* resid;
-  void* out;
-  int M, N, K, epi;
+  GemmArgs args;
+  int epi;
 };
 int gemm_block_n(int N);
 bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);

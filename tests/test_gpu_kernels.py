@@ -134,3 +134,27 @@ def test_fc_f32_parity(cuda_lib, n, N, K):
         if relu:
             ref = np.maximum(ref, 0)
         np.testing.assert_allclose(to_np(Y), ref, rtol=2e-5, atol=2e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 768, 768), (1000, 768, 3072), (129, 1024, 1024), (129, 1024, 4096),
+                                   (77, 128, 128), (200, 128, 512), (1, 768, 768), (5000, 768, 768)])
+def test_gemm_fused_residual_layernorm_parity(cuda_lib, M, N, K):
+    """Attention-output / FFN2 GEMM with the cluster-fused residual + LayerNorm epilogue
+    (row statistics exchanged over DSMEM) vs oracle linear -> + residual -> layer_norm."""
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(M + N + K)
+    A, A64 = bf16_tensor(rng.normal(0, 1, (M, K)))
+    W, W64 = bf16_tensor(rng.normal(0, 0.03, (N, K)))
+    b = rng.normal(0, 0.1, N).astype(np.float32)
+    res = rng.normal(0.2, 1.5, (M, N)).astype(np.float32)
+    g = (1 + rng.uniform(-0.1, 0.1, N)).astype(np.float32)
+    be = rng.normal(0, 0.02, N).astype(np.float32)
+    h = torch.from_numpy(res.copy()).cuda()
+    hb = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    binding.op_gemm_ln(A, W, torch.from_numpy(b).cuda(), h, torch.from_numpy(g).cuda(), torch.from_numpy(be).cuda(),
+                       1e-12, hb)
+    torch.cuda.synchronize()
+    ref = oenc.layer_norm(oenc.linear(A64, W64, b) + res, g, be, 1e-12)
+    np.testing.assert_allclose(to_np(h), ref, rtol=0, atol=2e-4)
+    np.testing.assert_allclose(to_np(hb), ref, rtol=8e-3, atol=1e-5)
