@@ -42,12 +42,18 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int CHUNKS_PER_WARP = BN / 64;  // 32-column chunks per epilogue warp
-  // barriers + LN scratch: stats[2 slots][kMaxCluster][128] float2 + part[2][128] float2
-  static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + AUX_BYTES;
+};
+// Shared-memory plan.  RES (the epilogue reads an fp32 residual) trades one operand stage for
+// a per-warp double-buffered residual staging area filled by cp.async ahead of use.
+template <int BN, bool RES>
+struct SmemPlan {
+  static constexpr int STAGES = RES ? (BN == 256 ? 3 : 4) : (BN == 256 ? 4 : 6);
+  static constexpr int RES_BYTES = RES ? kEpiWarps * 2 * 32 * 32 * 4 : 0;      // [warp][2][32 rows][32 f32]
+  // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta[256] f32
+  static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 3 * 256 * 4;
+  static constexpr int SMEM_BYTES = STAGES * GemmCfg<BN>::STAGE_BYTES + RES_BYTES + AUX_BYTES + 1024;
 };
 
 ELIS_DEV float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.7071067811865476f)); }
@@ -66,20 +72,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
   using C = GemmCfg<BN>;
   constexpr bool LN = (EPI == EPI_BIAS_RESID_LN);
+  constexpr bool RES = LN || (EPI == EPI_BIAS_RESID_F32);
+  using SP = SmemPlan<BN, RES>;
+  constexpr int STAGES = SP::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* aux = sB + C::STAGES * C::B_BYTES;
+  uint8_t* sB = smem + STAGES * C::A_BYTES;
+  float* res_base = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
+  uint8_t* aux = reinterpret_cast<uint8_t*>(res_base) + SP::RES_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;  // LN: stats slots filled by every CTA of the cluster
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + 2);
   float2* stats = reinterpret_cast<float2*>(aux + 512);         // [2][kMaxCluster][128]
   float2* part = stats + 2 * kMaxCluster * 128;                  // [2 halves][128]
+  float* sbias = reinterpret_cast<float*>(part + 2 * 128);        // [256]
+  float* sgam = sbias + 256;                                      // [256]
+  float* sbet = sgam + 256;                                       // [256]
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -100,7 +113,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
           tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m * BM);
           tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n * BN);
-          if (++s == C::STAGES) { s = 0; ph ^= 1u; }
+          if (++s == STAGES) { s = 0; ph ^= 1u; }
         }
       }
     }
@@ -158,55 +171,94 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tc_mma_f16(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit(&empty[s]);
-          if (++s == C::STAGES) { s = 0; ph ^= 1u; }
+          if (++s == STAGES) { s = 0; ph ^= 1u; }
         }
         tc_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global
+    constexpr int CH = C::CHUNKS_PER_WARP;
+    const int ew = warp - 4;             // 0..7
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = (warp - 4) >> 2;    // which half of the tile's columns
+    const int half = ew >> 2;            // which half of the tile's columns
     const int row_in_tile = q * 32 + lane;
+    const int etid = ew * 32 + lane;     // 0..255
+    float* rbuf = res_base + ew * (2 * 32 * 32) + lane * 32;   // this thread's row in buffer 0
+    auto stage_vectors = [&](int n) {    // bias (+ gamma, beta) of tile columns -> shared memory
+      if (etid < BN) {
+        sbias[etid] = __ldg(args.bias + n * BN + etid);
+        if constexpr (LN) {
+          sgam[etid] = __ldg(args.gamma + n * BN + etid);
+          sbet[etid] = __ldg(args.beta + n * BN + etid);
+        }
+      }
+    };
+    // residual chunk c of this thread's row -> buffer (c & 1), 16-byte pieces XOR-swizzled by row
+    auto prefetch_res = [&](int row, int col0, int c) {
+      const float* src = args.resid + static_cast<size_t>(row) * N + col0;
+      float* dst = rbuf + (c & 1) * (32 * 32);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cp_async16(dst + ((k ^ (lane & 7)) * 4), src + 4 * k, true);
+    };
+    if constexpr (LN) {
+      stage_vectors(rank);
+      named_bar_sync(1, kEpiWarps * 32);
+    }
     int it = 0;
     for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
       int m, n;
       tile_mn(t, m, n);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
       const int row = m * BM + row_in_tile;
       const bool row_ok = row < M;
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
       const int cbase = half * (BN / 2);  // first tile column of this warp
+      if constexpr (RES) {                // residual does not depend on the MMA: fetch it now
+#pragma unroll
+        for (int c = 0; c < 2 && c < CH; ++c) {
+          if (row_ok) prefetch_res(row, n * BN + cbase + c * 32, c);
+          cp_async_commit();
+        }
+      }
+      if constexpr (!LN) {
+        named_bar_sync(1, kEpiWarps * 32);  // previous tile's readers of sbias are done
+        stage_vectors(n);
+        named_bar_sync(1, kEpiWarps * 32);
+      }
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cbase;
       float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // LN row statistics over this warp's columns
-#pragma unroll 1
-      for (int c = 0; c < C::CHUNKS_PER_WARP; ++c) {
+      uint32_t r[2][32];
+      tmem_ld_32x32b_x32(taddr, r[0]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        tc_wait_ld();
+        if (c + 1 < CH) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
         const int tcol = cbase + c * 32;
         const int col0 = n * BN + tcol;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + tcol, r);
-        tc_wait_ld();
         float v[32];
-        const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 bb = __ldg(b4 + j);
-          v[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bb.x;
-          v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
-          v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
-          v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
+        for (int j = 0; j < 32; j += 4) {
+          const float4 bb = *reinterpret_cast<const float4*>(sbias + tcol + j);
+          v[j + 0] = __uint_as_float(r[c & 1][j + 0]) + bb.x;
+          v[j + 1] = __uint_as_float(r[c & 1][j + 1]) + bb.y;
+          v[j + 2] = __uint_as_float(r[c & 1][j + 2]) + bb.z;
+          v[j + 3] = __uint_as_float(r[c & 1][j + 3]) + bb.w;
         }
-        if constexpr (EPI == EPI_BIAS_RESID_F32 || LN) {
+        if constexpr (RES) {
+          if (c + 1 < CH) cp_async_wait<1>(); else cp_async_wait<0>();
           if (row_ok) {
-            const float4* r4 = reinterpret_cast<const float4*>(args.resid + static_cast<size_t>(row) * N + col0);
+            const float* src = rbuf + (c & 1) * (32 * 32);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 rr = __ldg(r4 + j);
-              v[4 * j] += rr.x; v[4 * j + 1] += rr.y; v[4 * j + 2] += rr.z; v[4 * j + 3] += rr.w;
+            for (int k = 0; k < 8; ++k) {
+              const float4 rr = *reinterpret_cast<const float4*>(src + ((k ^ (lane & 7)) * 4));
+              v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
             }
+            if (c + 2 < CH) prefetch_res(row, col0 + 64, c + 2);
           }
+          if (c + 2 < CH) cp_async_commit();
         }
         if constexpr (LN) {
           // chunk statistics, merged into the running (n, mean, M2); v kept in TMEM
@@ -219,9 +271,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int j = 0; j < 32; ++j) { const float d = v[j] - cm; m2 = fmaf(d, d, m2); }
           if (c == 0) { st_n = 32.f; st_mean = cm; st_m2 = m2; }
           else chan_merge(st_n, st_mean, st_m2, 32.f, cm, m2);
+          uint32_t w[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
-          tmem_st_32x32b_x32(taddr + tcol, r);
+          for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+          tmem_st_32x32b_x32(taddr + c * 32, w);
         } else if (row_ok) {
           if constexpr (EPI == EPI_BIAS_RESID_F32) {
             float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
@@ -245,7 +298,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int slot = it & 1;
         const uint32_t sph = (it >> 1) & 1;
         part[half * 128 + row_in_tile] = make_float2(st_mean, st_m2);
-        named_bar_sync(1, kEpiWarps * 32);
+        named_bar_sync(2, kEpiWarps * 32);
         if (half == 0) {
           // this CTA's statistics over its BN columns -> every CTA of the cluster
           float cn = st_n, cmean = st_mean, cm2 = st_m2;
@@ -267,24 +320,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           else chan_merge(tn, tmean, tm2, static_cast<float>(BN), s2.x, s2.y);
         }
         const float rstd = 1.0f / sqrtf(tm2 / tn + args.eps);
-#pragma unroll 1
-        for (int c = 0; c < C::CHUNKS_PER_WARP; ++c) {
+        tmem_ld_32x32b_x32(taddr, r[0]);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          tc_wait_ld();
+          if (c + 1 < CH) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
           const int tcol = cbase + c * 32;
           const int col0 = n * BN + tcol;
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + tcol, r);
-          tc_wait_ld();
           if (row_ok) {
             float y[32];
-            const float4* g4 = reinterpret_cast<const float4*>(args.gamma + col0);
-            const float4* be4 = reinterpret_cast<const float4*>(args.beta + col0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 g = __ldg(g4 + j), be = __ldg(be4 + j);
-              y[4 * j + 0] = (__uint_as_float(r[4 * j + 0]) - tmean) * rstd * g.x + be.x;
-              y[4 * j + 1] = (__uint_as_float(r[4 * j + 1]) - tmean) * rstd * g.y + be.y;
-              y[4 * j + 2] = (__uint_as_float(r[4 * j + 2]) - tmean) * rstd * g.z + be.z;
-              y[4 * j + 3] = (__uint_as_float(r[4 * j + 3]) - tmean) * rstd * g.w + be.w;
+            for (int j = 0; j < 32; j += 4) {
+              const float4 g = *reinterpret_cast<const float4*>(sgam + tcol + j);
+              const float4 be = *reinterpret_cast<const float4*>(sbet + tcol + j);
+              y[j + 0] = (__uint_as_float(r[c & 1][j + 0]) - tmean) * rstd * g.x + be.x;
+              y[j + 1] = (__uint_as_float(r[c & 1][j + 1]) - tmean) * rstd * g.y + be.y;
+              y[j + 2] = (__uint_as_float(r[c & 1][j + 2]) - tmean) * rstd * g.z + be.z;
+              y[j + 3] = (__uint_as_float(r[c & 1][j + 3]) - tmean) * rstd * g.w + be.w;
             }
             float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
 #pragma unroll
@@ -311,7 +363,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 template <int BN, int EPI>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  using C = SmemPlan<BN, EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID_F32>;
   auto kern = k_gemm_tc<BN, EPI>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
   if (e != cudaSuccess) return e;

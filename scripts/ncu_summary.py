@@ -82,8 +82,31 @@ def launches(path):
         print(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.2f} | {v / s:.3f} |")
 
 
+def hot(path, kernel_substr, top=25):
+    """Top SASS instructions by warp-stall samples for the first kernel matching kernel_substr."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+    blocks = raw.split('"Kernel Name",')
+    for b in blocks[1:]:
+        name = b.split("\n", 1)[0]
+        if kernel_substr not in name:
+            continue
+        rows = list(csv.reader(io.StringIO(b.split("\n", 1)[1])))
+        hdr = rows[0]
+        i_src, i_s = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
+        reasons = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+        tot = sum(float(r[i_s] or 0) for r in rows[1:] if len(r) > i_s)
+        print(name[:100], "total samples", tot)
+        best = sorted(rows[1:], key=lambda r: -float(r[i_s] or 0) if len(r) > i_s else 0)[:top]
+        for r in best:
+            rs = sorted(((float(r[i] or 0), hdr[i]) for i in reasons), reverse=True)[:2]
+            print(f"{float(r[i_s]) / tot:6.3f}  {r[i_src][:70]:70s} {rs}")
+        return
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "--launches":
+    if sys.argv[1] == "--hot":
+        hot(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "--launches":
         launches(sys.argv[2])
     else:
         full(sys.argv[1])
