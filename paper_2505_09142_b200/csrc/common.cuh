@@ -215,6 +215,11 @@ ELIS_DEV void st_cluster_f32x2(uint32_t addr, float a, float b) {
 ELIS_DEV void mbar_arrive_remote_release(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
+// Relaxed remote arrive: no memory fence (MEMBAR.ALL.GPU) -- for signals that only order
+// tcgen05 operations already completed by the caller (e.g. TMEM reads after wait::ld).
+ELIS_DEV void mbar_arrive_remote_relaxed(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
 ELIS_DEV void mbar_wait_acquire_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(

@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps * 32);  // both CTAs' epilogue threads (leader's copy used)
-      mbar_init(&sfull[a], 128 * cpairs);
+      mbar_init(&tempty[a], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs (leader's copy used)
+      mbar_init(&sfull[a], 4 * cpairs);      // one arrive per half-0 epilogue warp of every row peer
     }
     fence_mbar_init();
   }
@@ -336,13 +336,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           chan_merge(cn, cmean, cm2, st_n, o.x, o.y);
           const uint32_t lslot = smem_u32(&stats[(slot * kMaxCluster + pair_in_cluster) * 128 + row_in_tile]);
           const uint32_t lbar = smem_u32(&sfull[slot]);
-          for (int pp = 0; pp < cpairs; ++pp) {
-            const uint32_t peer = static_cast<uint32_t>(2 * pp + hrow);
-            st_cluster_f32x2(mapa_shared(lslot, peer), cmean, cm2);
-            mbar_arrive_remote_release(mapa_shared(lbar, peer));
-          }
+          for (int pp = 0; pp < cpairs; ++pp)
+            st_cluster_f32x2(mapa_shared(lslot, static_cast<uint32_t>(2 * pp + hrow)), cmean, cm2);
+          __syncwarp();
+          if (lane == 0)  // release is cumulative over the warp's DSMEM stores ordered by __syncwarp
+            for (int pp = 0; pp < cpairs; ++pp)
+              mbar_arrive_remote_release(mapa_shared(lbar, static_cast<uint32_t>(2 * pp + hrow)));
         }
-        mbar_wait_acquire_cluster(&sfull[slot], sph);
+        if (lane == 0) mbar_wait_acquire_cluster(&sfull[slot], sph);
+        __syncwarp();
         // merge the cpairs partials in pair order (identical on every CTA) -> mean, rstd
         float tn = 0.f, tmean = 0.f, tm2 = 0.f;
         for (int p = 0; p < cpairs; ++p) {
@@ -381,7 +383,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive_remote_release(tempty_leader + acc * 8);  // accumulator free (counted at the leader)
+      __syncwarp();
+      // accumulator free: every lane's tcgen05.ld completed (wait::ld), so a relaxed arrive suffices
+      if (lane == 0) mbar_arrive_remote_relaxed(tempty_leader + acc * 8);
     }
   }
   tc_fence_before();
