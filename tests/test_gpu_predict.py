@@ -194,3 +194,27 @@ def test_cfg2_full_size_sampled_parity(cuda_lib):
         o_ids, _, _, _ = isrtf_select(gpu, gen, cap)
         np.testing.assert_array_equal(ids.cpu().numpy(), o_ids)
     P.close()
+
+
+def test_cfg3_large_4096_ragged_sampled_parity(cuda_lib):
+    """BASELINE.json configs[2]: BGE-large re-predicting 4,096 ragged requests of 32-512
+    tokens (uniform lengths, T ~ 1.1M) in one call; stratified sample vs the oracle, the
+    whole batch finite, and the batch invariance of a sampled request."""
+    from oracle import head as ohead
+    n = 4096
+    L = inputs.uniform_lengths(n, 32, 512, seed=0)
+    tokens = inputs.make_tokens(L, seed=7)
+    cfg, W, P = make_predictor("large", int(L.sum()), n)
+    gpu, _ = run_predict(P, L, tokens)
+    assert np.isfinite(gpu).all()
+    order = np.argsort(L)
+    sample = sorted(set(order[np.linspace(0, n - 1, 4).astype(int)].tolist()))
+    ref = ohead.predict(tokens, L, W, cfg, requests=sample)
+    r = rel_err(gpu[sample], ref)
+    print("cfg3 sampled rel err", r.max(), "lengths", L[sample])
+    assert r.max() <= PRED_RTOL
+    starts = inputs.offsets(L)
+    i = sample[-1]
+    alone, _ = run_predict(P, L[i:i + 1], tokens[starts[i]:starts[i + 1]])
+    assert alone[0] == gpu[i]
+    P.close()
