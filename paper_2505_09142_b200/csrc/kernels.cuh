@@ -31,16 +31,19 @@ struct GemmPlan {
 };
 int gemm_block_n(int N);
 bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// bf16 [rows, cols] row-major, box {box_cols (<= 64 for SWIZZLE_128B), box_rows}, SWIZZLE_128B
+bool make_tmap_bf16_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                        uint32_t box_rows);
 // A: [a_rows >= M, K] bf16 (rows M..a_rows-1 are read but their outputs are not stored)
 bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
                     const float* resid, void* out, int M, int N, int K, int epi);
 cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st);
 
 // ---- varlen metadata / embedding / LayerNorm (norm.cu)
-constexpr int kAttnTileQ = 64;
-// lengths[n] -> cu_seqlens[n+1], attention work list (request, q0) and its size; validates.
+// lengths[n] -> cu_seqlens[n+1], attention work list (request, q0) with q tiles of tile_q
+// rows, and its size; validates lengths and their sum.
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        int2* work, int32_t* num_work, uint32_t* err, cudaStream_t st);
+                        int2* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st);
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
                             int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
                             const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
@@ -49,11 +52,15 @@ cudaError_t launch_layernorm(const float* u, const float* gamma, const float* be
                              float* out32, uint16_t* outb, cudaStream_t st);
 
 // ---- attention (attention.cu)
+// head dim 64: tcgen05 kernel with 128-row q tiles (needs the qkv tensor map); 32: mma.sync, 64 rows.
+inline int attn_tile_q(int head_dim) { return head_dim == 64 ? 128 : 64; }
 // grid upper bound on the number of q-tiles for T tokens in n requests
-inline int64_t attn_max_tiles(int64_t T, int n) { return (T + kAttnTileQ - 1) / kAttnTileQ + n; }
-cudaError_t launch_attention(const uint16_t* qkv, const int32_t* cu_seqlens, const int2* work,
-                             const int32_t* num_work, int64_t max_tiles, int H, int num_heads, uint16_t* ctx,
-                             cudaStream_t st);
+inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q - 1) / tile_q + n; }
+// qkv [rows, 3H] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
+bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
+cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
+                             const int2* work, const int32_t* num_work, int64_t max_tiles, int H, int num_heads,
+                             uint16_t* ctx, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,

@@ -48,7 +48,7 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total_out) {
 __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict__ lengths, int n, long long total,
                                                        int max_position, int32_t* __restrict__ cu,
                                                        int2* __restrict__ work, int32_t* __restrict__ num_work,
-                                                       uint32_t* __restrict__ err) {
+                                                       uint32_t* __restrict__ err, int tile_q) {
   __shared__ int warp_tot[32];
   __shared__ int s_total_len, s_total_tiles;
   __shared__ uint32_t s_err;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict
     int L = lengths[i];
     if (L < 1 || L > max_position) { e |= ERR_LENGTH; L = max(1, min(L, max_position)); }
     my_len += L;
-    my_tiles += (L + kAttnTileQ - 1) / kAttnTileQ;
+    my_tiles += (L + tile_q - 1) / tile_q;
   }
   if (e) atomicOr(&s_err, e);
   const int len_off = block_exclusive_scan(my_len, warp_tot, &s_total_len);
@@ -75,8 +75,8 @@ __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict
     int L = max(1, min(lengths[i], max_position));
     cu[i] = lo;
     if (ok) {
-      const int nt = (L + kAttnTileQ - 1) / kAttnTileQ;
-      for (int t = 0; t < nt; ++t) work[to + t] = make_int2(i, t * kAttnTileQ);
+      const int nt = (L + tile_q - 1) / tile_q;
+      for (int t = 0; t < nt; ++t) work[to + t] = make_int2(i, t * tile_q);
       to += nt;
     }
     lo += L;
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ u, 
 }  // namespace
 
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        int2* work, int32_t* num_work, uint32_t* err, cudaStream_t st) {
-  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err);
+                        int2* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st) {
+  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err, tile_q);
   return cudaGetLastError();
 }
 
