@@ -190,7 +190,6 @@ __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ 
       *reinterpret_cast<uint32_t*>(out + static_cast<size_t>(r1) * H + col) = pack_bf16x2(o[dt][2] * inv1, o[dt][3] * inv1);
   }
 }
-
 // ============================================================================ tcgen05 engine
 // One CTA = (request, head, 128-row q tile), head dim 64.  BERT requests are <= 512 tokens,
 // so a whole score row (<= 512 fp32) fits in tensor memory: the softmax is computed EXACTLY
@@ -203,27 +202,36 @@ __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ 
 //      into TMEM columns [0, Lk/2) (in place: chunk c's P lands on already-consumed S);
 //   4. O = P V on tcgen05 with A = P read from TMEM and B = V (MN-major) from shared memory;
 //   5. ctx = O / rowsum -> bf16.
-// TMEM: 512 columns (S, then P in [0,256) and O in [256,320)); shared: 144 KB.
+// Requests are bucketed by length (<= 128, <= 256, <= 512 keys: NKB = 1, 2, 4 key blocks) and
+// each bucket is its own launch sized to it: TMEM NKB x 128 columns (S; then P in
+// [0, 64 NKB) and O in [64 NKB, 64 NKB + 64)) and (1 + 2 NKB) x 16 KB of shared memory, so
+// 4 / 2 / 1 CTAs share an SM and one CTA's loads and MMAs overlap another's softmax.
 constexpr int TQ = 128;        // q rows per CTA (= TMEM lanes)
 constexpr int TKB = 128;       // keys per K/V block
 constexpr int TD = 64;         // head dim
-constexpr int kMaxKeyBlocks = 4;
 constexpr int kBlkBytes = TKB * TD * 2;  // 16 KB
-constexpr int kAttnTcSmem = (1 + 2 * kMaxKeyBlocks) * kBlkBytes + 1024 + 256;
-constexpr uint32_t kOCol = 256;
+template <int NKB>
+struct AttnTc {
+  static constexpr int SMEM = (1 + 2 * NKB) * kBlkBytes + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = NKB * 128;
+  static constexpr uint32_t O_COL = NKB * 64;
+  static constexpr int MAX_CHUNKS = NKB * (TKB / 32);
+};
 
-__global__ void __launch_bounds__(256, 1)
+template <int NKB>
+__global__ void __launch_bounds__(128)
     k_attention_tc(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ cu,
                    const int2* __restrict__ work, const int32_t* __restrict__ num_work, int H,
                    uint16_t* __restrict__ ctx, float scale_log2) {
+  using C = AttnTc<NKB>;
   if (static_cast<int>(blockIdx.x) >= __ldg(num_work)) return;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + kBlkBytes;
-  uint8_t* sV = sK + kMaxKeyBlocks * kBlkBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kMaxKeyBlocks * kBlkBytes);
+  uint8_t* sV = sK + NKB * kBlkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NKB * kBlkBytes);
   uint64_t* qk_full = bars + 0;
   uint64_t* v_full = bars + 1;
   uint64_t* s_full = bars + 2;
@@ -236,111 +244,117 @@ __global__ void __launch_bounds__(256, 1)
   const int start = __ldg(cu + req);
   const int L = __ldg(cu + req + 1) - start;
   const int h = blockIdx.y;
-  const int nkb = (L + TKB - 1) / TKB;  // 1..4
+  const int nkb = (L + TKB - 1) / TKB;  // <= NKB by construction of the bucket
   const int warp = warp_id(), lane = lane_id();
 
+  // One group of 4 warps: thread 0 issues the TMA loads and both MMA phases in program order;
+  // every thread (= query row = TMEM lane) runs the softmax and the epilogue.
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
     mbar_init(qk_full, 1);
     mbar_init(v_full, 1);
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  if (warp == 0) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  (void)p_full;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(qk_full, (1 + nkb) * kBlkBytes);
-      tma_load_2d(sQ, &tm, qk_full, h * TD, start + q0);
-      for (int j = 0; j < nkb; ++j) tma_load_2d(sK + j * kBlkBytes, &tm, qk_full, H + h * TD, start + j * TKB);
-      mbar_arrive_expect_tx(v_full, nkb * kBlkBytes);
-      for (int j = 0; j < nkb; ++j) tma_load_2d(sV + j * kBlkBytes, &tm, v_full, 2 * H + h * TD, start + j * TKB);
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // S = Q K^T: M 128, N 128 per key block, K 64 (4 x K16, +32 B per step in the 128 B swizzle row)
-      mbar_wait(qk_full, 0);
-      tc_fence_after();
-      constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
-      const uint64_t dq = make_sw128_desc(smem_u32(sQ));
-      for (int j = 0; j < nkb; ++j) {
-        const uint64_t dk = make_sw128_desc(smem_u32(sK + j * kBlkBytes));
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(qk_full, (1 + nkb) * kBlkBytes);
+    tma_load_2d(sQ, &tm, qk_full, h * TD, start + q0);
+    for (int j = 0; j < nkb; ++j) tma_load_2d(sK + j * kBlkBytes, &tm, qk_full, H + h * TD, start + j * TKB);
+    mbar_arrive_expect_tx(v_full, nkb * kBlkBytes);
+    for (int j = 0; j < nkb; ++j) tma_load_2d(sV + j * kBlkBytes, &tm, v_full, 2 * H + h * TD, start + j * TKB);
+    // S = Q K^T: M 128, N 128 per key block, K 64 (4 x K16, +32 B per step in the 128 B swizzle row)
+    mbar_wait(qk_full, 0);
+    tc_fence_after();
+    constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
+    const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+    for (int j = 0; j < nkb; ++j) {
+      const uint64_t dk = make_sw128_desc(smem_u32(sK + j * kBlkBytes));
 #pragma unroll
-        for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem + j * TKB, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
-      }
-      tc_commit(s_full);
-      // O = P V: A = P from TMEM (8 columns of bf16 pairs per K16), B = V MN-major (16 keys = 2 KB)
-      mbar_wait(p_full, 0);
-      mbar_wait(v_full, 0);
-      tc_fence_after();
-      constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B major = MN
-      const int nks = nkb * (TKB / 16);
-      for (int ks = 0; ks < nks; ++ks) {
-        const uint64_t dv = make_sw128_desc(smem_u32(sV + ks * (16 * TD * 2)));
-        tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, ks > 0);
-      }
-      tc_commit(o_full);
+      for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem + j * TKB, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
     }
-  } else if (warp >= 4) {
-    const int q = warp - 4;
+    tc_commit(s_full);
+  }
+  {
+    const int q = warp;
     const int row = q * 32 + lane;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int nchunks = nkb * (TKB / 32);
     mbar_wait(s_full, 0);
     tc_fence_after();
-    // pass A: row max of the scaled scores over the request's keys
+    uint32_t r[2][32];
+    // pass A: row max of the scaled scores over the request's keys (TMEM loads double-buffered)
     float mx = -INFINITY;
-    for (int c = 0; c < nchunks; ++c) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(taddr + c * 32, r);
-      tc_wait_ld();
-      const int nvalid = L - c * 32;  // keys >= L belong to other requests: masked
+    tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid) mx = fmaxf(mx, __uint_as_float(r[j]) * scale_log2);
+    for (int c = 0; c < C::MAX_CHUNKS; ++c) {
+      if (c < nchunks) {
+        tc_wait_ld();
+        if (c + 1 < nchunks) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
+        const int nvalid = L - c * 32;  // keys >= L belong to other requests: masked
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nvalid) mx = fmaxf(mx, __uint_as_float(r[c & 1][j]));
+      }
     }
+    const float mxs = mx * scale_log2;
     // pass B: p = exp2(s*scale - max), row sum, P (bf16 pairs) written over consumed S columns
     float l = 0.f;
-    for (int c = 0; c < nchunks; ++c) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(taddr + c * 32, r);
-      tc_wait_ld();
-      const int nvalid = L - c * 32;
-      uint32_t pk[16];
+    tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float p0, p1;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[j]), scale_log2, -mx)));
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[j + 1]), scale_log2, -mx)));
-        p0 = (j < nvalid) ? p0 : 0.f;
-        p1 = (j + 1 < nvalid) ? p1 : 0.f;
-        l += p0 + p1;
-        pk[j / 2] = pack_bf16x2(p0, p1);
+    for (int c = 0; c < C::MAX_CHUNKS; ++c) {
+      if (c < nchunks) {
+        tc_wait_ld();
+        if (c + 1 < nchunks) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
+        const int nvalid = L - c * 32;
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float p0, p1;
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[c & 1][j]), scale_log2, -mxs)));
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[c & 1][j + 1]), scale_log2, -mxs)));
+          p0 = (j < nvalid) ? p0 : 0.f;
+          p1 = (j + 1 < nvalid) ? p1 : 0.f;
+          l += p0 + p1;
+          pk[j / 2] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x32b_x16(taddr + c * 16, pk);
       }
-      tmem_st_32x32b_x16(taddr + c * 16, pk);
     }
     tc_wait_st();
     tc_fence_before();
-    mbar_arrive(p_full);
+    __syncthreads();  // P complete in TMEM (all 128 rows)
+    if (threadIdx.x == 0) {
+      // O = P V: A = P from TMEM (8 columns of bf16 pairs per K16), B = V MN-major (16 keys = 2 KB)
+      tc_fence_after();
+      mbar_wait(v_full, 0);
+      constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B major = MN
+      const int nks = nkb * (TKB / 16);
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t dv = make_sw128_desc(smem_u32(sV + ks * (16 * TD * 2)));
+        tc_mma_f16_tmem_a(tmem + C::O_COL, tmem + ks * 8, dv, idesc_o, ks > 0);
+      }
+      tc_commit(o_full);
+    }
     // epilogue: O / l -> bf16 ctx
     mbar_wait(o_full, 0);
     tc_fence_after();
-    uint32_t o[2][32];
-    tmem_ld_32x32b_x32(taddr + kOCol, o[0]);
-    tmem_ld_32x32b_x32(taddr + kOCol + 32, o[1]);
+    tmem_ld_32x32b_x32(taddr + C::O_COL, r[0]);
+    tmem_ld_32x32b_x32(taddr + C::O_COL + 32, r[1]);
     tc_wait_ld();
     if (q0 + row < L) {
       const float inv = 1.0f / l;
       uint4* dst = reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + row) * H + h * TD);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const uint32_t* s = o[k >> 2] + (k & 3) * 8;
+        const uint32_t* s = r[k >> 2] + (k & 3) * 8;
         dst[k] = make_uint4(pack_bf16x2(__uint_as_float(s[0]) * inv, __uint_as_float(s[1]) * inv),
                             pack_bf16x2(__uint_as_float(s[2]) * inv, __uint_as_float(s[3]) * inv),
                             pack_bf16x2(__uint_as_float(s[4]) * inv, __uint_as_float(s[5]) * inv),
@@ -350,10 +364,22 @@ __global__ void __launch_bounds__(256, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<C::TMEM_COLS>(tmem);
   }
+}
+
+template <int NKB>
+cudaError_t launch_tc_bucket(const CUtensorMap& tm, const int32_t* cu, const int2* work, const int32_t* num_work,
+                             int64_t grid_x, int H, int num_heads, uint16_t* ctx, float scale_log2, cudaStream_t st) {
+  if (grid_x <= 0) return cudaSuccess;
+  using C = AttnTc<NKB>;
+  cudaError_t e = cudaFuncSetAttribute(k_attention_tc<NKB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  dim3 grid(static_cast<unsigned>(grid_x), static_cast<unsigned>(num_heads));
+  k_attention_tc<NKB><<<grid, 128, C::SMEM, st>>>(tm, cu, work, num_work, H, ctx, scale_log2);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -364,18 +390,28 @@ bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
 }
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
-                             const int2* work, const int32_t* num_work, int64_t max_tiles, int H, int num_heads,
+                             const int2* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
                              uint16_t* ctx, cudaStream_t st) {
-  if (max_tiles <= 0) return cudaSuccess;
+  if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
-  dim3 grid(static_cast<unsigned>(max_tiles), static_cast<unsigned>(num_heads));
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
+    const int64_t cap = attn_bucket_capacity(T, n);
+    cudaError_t e;
+    // longest bucket first: its 1-CTA-per-SM tiles start early, short tiles fill the tail
+    e = launch_tc_bucket<4>(*tm_qkv, cu_seqlens, work + 2 * cap, num_work + 2, attn_bucket_grid(T, n, 2), H,
+                            num_heads, ctx, scale_log2, st);
     if (e != cudaSuccess) return e;
-    k_attention_tc<<<grid, 256, kAttnTcSmem, st>>>(*tm_qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
-  } else if (d == 32) {
+    e = launch_tc_bucket<2>(*tm_qkv, cu_seqlens, work + cap, num_work + 1, attn_bucket_grid(T, n, 1), H, num_heads,
+                            ctx, scale_log2, st);
+    if (e != cudaSuccess) return e;
+    return launch_tc_bucket<1>(*tm_qkv, cu_seqlens, work, num_work, attn_bucket_grid(T, n, 0), H, num_heads, ctx,
+                               scale_log2, st);
+  }
+  const int64_t max_tiles = (T + BQ - 1) / BQ + n;
+  dim3 grid(static_cast<unsigned>(max_tiles), static_cast<unsigned>(num_heads));
+  if (d == 32) {
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;

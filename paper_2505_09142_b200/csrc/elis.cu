@@ -376,9 +376,9 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   ALLOC(p->g, static_cast<size_t>(T) * F);
   ALLOC(p->cu, N + 1);
   p->tile_q = attn_tile_q(H / cfg->num_heads);
-  p->max_tiles = attn_max_tiles(T, N, p->tile_q);
+  p->max_tiles = attn_work_capacity(T, N, p->tile_q);
   ALLOC(p->work, p->max_tiles);
-  ALLOC(p->num_work, 1);
+  ALLOC(p->num_work, 3);
   ALLOC(p->err, 1);
   ALLOC(p->pooled, static_cast<size_t>(N) * H);
   ALLOC(p->z0, static_cast<size_t>(N) * cfg->head_hidden);
@@ -440,13 +440,13 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   LAUNCH(p, PC_EMBED, st,
          launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
                          p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err, st));
-  const int64_t tiles = attn_max_tiles(total_tokens, n, p->tile_q);
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     LAUNCH(p, PC_ATTN, st,
-           launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, tiles, H, c.num_heads, p->ctx, st));
+           launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, p->ctx,
+                            st));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
@@ -723,7 +723,7 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   if (d != 32 && d != 64) return fail(ELIS_ERR_INVALID_ARG, "head dim");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int tq = attn_tile_q(d);
-  const int64_t tiles = attn_max_tiles(T, n, tq);
+  const int64_t tiles = attn_work_capacity(T, n, tq);
   CUtensorMap tm{};
   if (d == 64 && !make_tmap_qkv(&tm, qkv, static_cast<uint64_t>(T), hidden))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
@@ -731,12 +731,12 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   int2* work = nullptr;
   uint32_t* err = nullptr;
   CUDA_TRY(cudaMalloc(&cu, (n + 1) * 4));
-  CUDA_TRY(cudaMalloc(&nw, 4));
+  CUDA_TRY(cudaMalloc(&nw, 3 * 4));
   CUDA_TRY(cudaMalloc(&err, 4));
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(int2)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, tiles, hidden, num_heads, ctx, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, ctx, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);
