@@ -191,51 +191,41 @@ __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ 
   }
 }
 // ============================================================================ tcgen05 engine
-// One CTA = (request, head, 128-row q tile), head dim 64.  BERT requests are <= 512 tokens,
-// so a whole score row (<= 512 fp32) fits in tensor memory: the softmax is computed EXACTLY
-// in two passes (row max, then exp2 / row sum) instead of the online rescaling a
-// long-context kernel needs.
-//   1. TMA: Q [128 x 64], K and V [128-key blocks x 64] (SWIZZLE_128B) of this head;
-//   2. S = Q K^T on tcgen05 (M 128, N 128 per key block, K 64) into TMEM columns [0, Lk);
-//   3. 4 softmax warps (thread = query row = TMEM lane): pass A row max over the request's
-//      keys, pass B p = exp2(s*scale - max), row sum, P packed to bf16 pairs written back
-//      into TMEM columns [0, Lk/2) (in place: chunk c's P lands on already-consumed S);
-//   4. O = P V on tcgen05 with A = P read from TMEM and B = V (MN-major) from shared memory;
-//   5. ctx = O / rowsum -> bf16.
-// Requests are bucketed by length (<= 128, <= 256, <= 512 keys: NKB = 1, 2, 4 key blocks) and
-// each bucket is its own launch sized to it: TMEM NKB x 128 columns (S; then P in
-// [0, 64 NKB) and O in [64 NKB, 64 NKB + 64)) and (1 + 2 NKB) x 16 KB of shared memory, so
-// 4 / 2 / 1 CTAs share an SM and one CTA's loads and MMAs overlap another's softmax.
+// One CTA (4 warps) = (request, head, 128-row q tile), head dim 64; thread = query row =
+// TMEM lane.  Keys are processed in blocks of 128 (<= 4 per request, BERT max 512 tokens):
+//   S_j = Q K_j^T        tcgen05 M 128 x N 128 x K 64, into TMEM columns [0, 128)
+//   softmax block j      2 passes over the TMEM row (block max, then exp2 / sum), online
+//                        rescaling of (m, l, O) with fp32 statistics; P_j packed to bf16
+//                        pairs into TMEM columns [0, 64) over consumed scores
+//   O_j = P_j V_j        tcgen05 with A = P_j from TMEM, B = V_j (MN-major) from shared memory,
+//                        into TMEM columns [64, 128); accumulated in registers as O = a O + O_j
+//   ctx = O / l          bf16
+// Thread 0 issues the TMA loads (K_{j+1} overlaps softmax j, V_{j+1} overlaps S_{j+1}) and
+// the MMAs.  128 TMEM columns and 48 KB of shared memory per CTA let several CTAs share an SM,
+// so one CTA's loads and MMAs overlap another's softmax.
 constexpr int TQ = 128;        // q rows per CTA (= TMEM lanes)
 constexpr int TKB = 128;       // keys per K/V block
 constexpr int TD = 64;         // head dim
 constexpr int kBlkBytes = TKB * TD * 2;  // 16 KB
-template <int NKB>
-struct AttnTc {
-  static constexpr int SMEM = (1 + 2 * NKB) * kBlkBytes + 1024 + 256;
-  static constexpr uint32_t TMEM_COLS = NKB * 128;
-  static constexpr uint32_t O_COL = NKB * 64;
-  static constexpr int MAX_CHUNKS = NKB * (TKB / 32);
-};
+constexpr int kAttnTcSmem = 3 * kBlkBytes + 1024 + 256;
+constexpr uint32_t kOCol = 64;
 
-template <int NKB>
 __global__ void __launch_bounds__(128)
     k_attention_tc(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ cu,
                    const int2* __restrict__ work, const int32_t* __restrict__ num_work, int H,
                    uint16_t* __restrict__ ctx, float scale_log2) {
-  using C = AttnTc<NKB>;
   if (static_cast<int>(blockIdx.x) >= __ldg(num_work)) return;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + kBlkBytes;
-  uint8_t* sV = sK + NKB * kBlkBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NKB * kBlkBytes);
-  uint64_t* qk_full = bars + 0;
-  uint64_t* v_full = bars + 1;
-  uint64_t* s_full = bars + 2;
-  uint64_t* p_full = bars + 3;
+  uint8_t* sV = sK + kBlkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kBlkBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = bars + 2;
+  uint64_t* s_full = bars + 3;
   uint64_t* o_full = bars + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
 
@@ -244,142 +234,143 @@ __global__ void __launch_bounds__(128)
   const int start = __ldg(cu + req);
   const int L = __ldg(cu + req + 1) - start;
   const int h = blockIdx.y;
-  const int nkb = (L + TKB - 1) / TKB;  // <= NKB by construction of the bucket
+  const int nkb = (L + TKB - 1) / TKB;  // 1..4
   const int warp = warp_id(), lane = lane_id();
+  const bool issuer = threadIdx.x == 0;
 
-  // One group of 4 warps: thread 0 issues the TMA loads and both MMA phases in program order;
-  // every thread (= query row = TMEM lane) runs the softmax and the epilogue.
-  if (warp == 0 && lane == 0) {
+  if (issuer) {
     tma_prefetch_desc(&tm);
-    mbar_init(qk_full, 1);
+    mbar_init(q_full, 1);
+    mbar_init(k_full, 1);
     mbar_init(v_full, 1);
     mbar_init(s_full, 1);
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 0) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  (void)p_full;
+  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int row = warp * 32 + lane;
 
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(qk_full, (1 + nkb) * kBlkBytes);
-    tma_load_2d(sQ, &tm, qk_full, h * TD, start + q0);
-    for (int j = 0; j < nkb; ++j) tma_load_2d(sK + j * kBlkBytes, &tm, qk_full, H + h * TD, start + j * TKB);
-    mbar_arrive_expect_tx(v_full, nkb * kBlkBytes);
-    for (int j = 0; j < nkb; ++j) tma_load_2d(sV + j * kBlkBytes, &tm, v_full, 2 * H + h * TD, start + j * TKB);
-    // S = Q K^T: M 128, N 128 per key block, K 64 (4 x K16, +32 B per step in the 128 B swizzle row)
-    mbar_wait(qk_full, 0);
-    tc_fence_after();
-    constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
-    const uint64_t dq = make_sw128_desc(smem_u32(sQ));
-    for (int j = 0; j < nkb; ++j) {
-      const uint64_t dk = make_sw128_desc(smem_u32(sK + j * kBlkBytes));
-#pragma unroll
-      for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem + j * TKB, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
-    }
-    tc_commit(s_full);
+  constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
+  constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B (V) is MN-major
+  if (issuer) {
+    mbar_arrive_expect_tx(q_full, kBlkBytes);
+    tma_load_2d(sQ, &tm, q_full, h * TD, start + q0);
+    mbar_arrive_expect_tx(k_full, kBlkBytes);
+    tma_load_2d(sK, &tm, k_full, H + h * TD, start);
+    mbar_arrive_expect_tx(v_full, kBlkBytes);
+    tma_load_2d(sV, &tm, v_full, 2 * H + h * TD, start);
+    mbar_wait(q_full, 0);
   }
-  {
-    const int q = warp;
-    const int row = q * 32 + lane;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int nchunks = nkb * (TKB / 32);
-    mbar_wait(s_full, 0);
+  float m = -INFINITY, l = 0.f;   // running row max (scaled, log2 domain) and row sum
+  float o[TD];
+#pragma unroll
+  for (int i = 0; i < TD; ++i) o[i] = 0.f;
+
+  for (int j = 0; j < nkb; ++j) {
+    const uint32_t ph = j & 1;
+    if (issuer) {
+      // S_j = Q K_j^T (4 x K16 steps, +32 B inside the 128 B swizzle row)
+      mbar_wait(k_full, ph);
+      tc_fence_after();
+      const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+      const uint64_t dk = make_sw128_desc(smem_u32(sK));
+#pragma unroll
+      for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+      tc_commit(s_full);
+    }
+    mbar_wait(s_full, ph);
     tc_fence_after();
+    if (issuer && j + 1 < nkb) {  // the S MMA has consumed K_j: prefetch K_{j+1}
+      mbar_arrive_expect_tx(k_full, kBlkBytes);
+      tma_load_2d(sK, &tm, k_full, H + h * TD, start + (j + 1) * TKB);
+    }
+    const int nvalid_blk = L - j * TKB;  // keys >= L belong to other requests: masked
+    // pass A: block max (TMEM loads double-buffered)
     uint32_t r[2][32];
-    // pass A: row max of the scaled scores over the request's keys (TMEM loads double-buffered)
-    float mx = -INFINITY;
+    float bm = -INFINITY;
     tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
-    for (int c = 0; c < C::MAX_CHUNKS; ++c) {
-      if (c < nchunks) {
-        tc_wait_ld();
-        if (c + 1 < nchunks) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
-        const int nvalid = L - c * 32;  // keys >= L belong to other requests: masked
+    for (int c = 0; c < TKB / 32; ++c) {
+      tc_wait_ld();
+      if (c + 1 < TKB / 32) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nvalid) mx = fmaxf(mx, __uint_as_float(r[c & 1][j]));
-      }
+      for (int e = 0; e < 32; ++e)
+        if (c * 32 + e < nvalid_blk) bm = fmaxf(bm, __uint_as_float(r[c & 1][e]));
     }
-    const float mxs = mx * scale_log2;
-    // pass B: p = exp2(s*scale - max), row sum, P (bf16 pairs) written over consumed S columns
-    float l = 0.f;
+    const float m_new = fmaxf(m, bm * scale_log2);  // finite: every block has >= 1 valid key
+    float alpha;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(alpha) : "f"(m - m_new));  // 0 on the first block
+    m = m_new;
+    // pass B: p = exp2(s*scale - m), block sum, P (bf16 pairs) over consumed score columns
+    float bl = 0.f;
     tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
-    for (int c = 0; c < C::MAX_CHUNKS; ++c) {
-      if (c < nchunks) {
-        tc_wait_ld();
-        if (c + 1 < nchunks) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
-        const int nvalid = L - c * 32;
-        uint32_t pk[16];
+    for (int c = 0; c < TKB / 32; ++c) {
+      tc_wait_ld();
+      if (c + 1 < TKB / 32) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
+      uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          float p0, p1;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[c & 1][j]), scale_log2, -mxs)));
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[c & 1][j + 1]), scale_log2, -mxs)));
-          p0 = (j < nvalid) ? p0 : 0.f;
-          p1 = (j + 1 < nvalid) ? p1 : 0.f;
-          l += p0 + p1;
-          pk[j / 2] = pack_bf16x2(p0, p1);
-        }
-        tmem_st_32x32b_x16(taddr + c * 16, pk);
+      for (int e = 0; e < 32; e += 2) {
+        float p0, p1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[c & 1][e]), scale_log2, -m)));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[c & 1][e + 1]), scale_log2, -m)));
+        p0 = (c * 32 + e < nvalid_blk) ? p0 : 0.f;
+        p1 = (c * 32 + e + 1 < nvalid_blk) ? p1 : 0.f;
+        bl += p0 + p1;
+        pk[e / 2] = pack_bf16x2(p0, p1);
       }
+      tmem_st_32x32b_x16(taddr + c * 16, pk);
     }
+    l = l * alpha + bl;
     tc_wait_st();
     tc_fence_before();
-    __syncthreads();  // P complete in TMEM (all 128 rows)
-    if (threadIdx.x == 0) {
-      // O = P V: A = P from TMEM (8 columns of bf16 pairs per K16), B = V MN-major (16 keys = 2 KB)
+    __syncthreads();  // P_j complete in TMEM (all 128 rows)
+    if (issuer) {
       tc_fence_after();
-      mbar_wait(v_full, 0);
-      constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B major = MN
-      const int nks = nkb * (TKB / 16);
-      for (int ks = 0; ks < nks; ++ks) {
+      mbar_wait(v_full, ph);
+#pragma unroll
+      for (int ks = 0; ks < TKB / 16; ++ks) {
         const uint64_t dv = make_sw128_desc(smem_u32(sV + ks * (16 * TD * 2)));
-        tc_mma_f16_tmem_a(tmem + C::O_COL, tmem + ks * 8, dv, idesc_o, ks > 0);
+        tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, ks > 0);
       }
       tc_commit(o_full);
     }
-    // epilogue: O / l -> bf16 ctx
-    mbar_wait(o_full, 0);
+    mbar_wait(o_full, ph);
     tc_fence_after();
-    tmem_ld_32x32b_x32(taddr + C::O_COL, r[0]);
-    tmem_ld_32x32b_x32(taddr + C::O_COL + 32, r[1]);
-    tc_wait_ld();
-    if (q0 + row < L) {
-      const float inv = 1.0f / l;
-      uint4* dst = reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + row) * H + h * TD);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t* s = r[k >> 2] + (k & 3) * 8;
-        dst[k] = make_uint4(pack_bf16x2(__uint_as_float(s[0]) * inv, __uint_as_float(s[1]) * inv),
-                            pack_bf16x2(__uint_as_float(s[2]) * inv, __uint_as_float(s[3]) * inv),
-                            pack_bf16x2(__uint_as_float(s[4]) * inv, __uint_as_float(s[5]) * inv),
-                            pack_bf16x2(__uint_as_float(s[6]) * inv, __uint_as_float(s[7]) * inv));
-      }
+    if (issuer && j + 1 < nkb) {  // the PV MMA has consumed V_j: prefetch V_{j+1}
+      mbar_arrive_expect_tx(v_full, kBlkBytes);
+      tma_load_2d(sV, &tm, v_full, 2 * H + h * TD, start + (j + 1) * TKB);
     }
+    tmem_ld_32x32b_x32(taddr + kOCol, r[0]);
+    tmem_ld_32x32b_x32(taddr + kOCol + 32, r[1]);
+    tc_wait_ld();
+#pragma unroll
+    for (int i = 0; i < TD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(r[i >> 5][i & 31]));
+    tc_fence_before();
+    __syncthreads();  // every row has read O_j before the next S MMA overwrites columns [0, 128)
+  }
+  // epilogue: ctx = O / l (bf16)
+  if (q0 + row < L) {
+    const float inv = 1.0f / l;
+    uint4* dst = reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + row) * H + h * TD);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      dst[k] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
+                          pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
+                          pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
+                          pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem);
+    tmem_dealloc<128>(tmem);
   }
-}
-
-template <int NKB>
-cudaError_t launch_tc_bucket(const CUtensorMap& tm, const int32_t* cu, const int2* work, const int32_t* num_work,
-                             int64_t grid_x, int H, int num_heads, uint16_t* ctx, float scale_log2, cudaStream_t st) {
-  if (grid_x <= 0) return cudaSuccess;
-  using C = AttnTc<NKB>;
-  cudaError_t e = cudaFuncSetAttribute(k_attention_tc<NKB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  if (e != cudaSuccess) return e;
-  dim3 grid(static_cast<unsigned>(grid_x), static_cast<unsigned>(num_heads));
-  k_attention_tc<NKB><<<grid, 128, C::SMEM, st>>>(tm, cu, work, num_work, H, ctx, scale_log2);
-  return cudaGetLastError();
 }
 
 }  // namespace
@@ -395,23 +386,14 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+  const int64_t max_tiles = attn_max_tiles(T, n, attn_tile_q(d));
+  dim3 grid(static_cast<unsigned>(max_tiles), static_cast<unsigned>(num_heads));
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
-    const int64_t cap = attn_bucket_capacity(T, n);
-    cudaError_t e;
-    // longest bucket first: its 1-CTA-per-SM tiles start early, short tiles fill the tail
-    e = launch_tc_bucket<4>(*tm_qkv, cu_seqlens, work + 2 * cap, num_work + 2, attn_bucket_grid(T, n, 2), H,
-                            num_heads, ctx, scale_log2, st);
+    cudaError_t e = cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
     if (e != cudaSuccess) return e;
-    e = launch_tc_bucket<2>(*tm_qkv, cu_seqlens, work + cap, num_work + 1, attn_bucket_grid(T, n, 1), H, num_heads,
-                            ctx, scale_log2, st);
-    if (e != cudaSuccess) return e;
-    return launch_tc_bucket<1>(*tm_qkv, cu_seqlens, work, num_work, attn_bucket_grid(T, n, 0), H, num_heads, ctx,
-                               scale_log2, st);
-  }
-  const int64_t max_tiles = (T + BQ - 1) / BQ + n;
-  dim3 grid(static_cast<unsigned>(max_tiles), static_cast<unsigned>(num_heads));
-  if (d == 32) {
+    k_attention_tc<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
+  } else if (d == 32) {
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;

@@ -52,23 +52,14 @@ cudaError_t launch_layernorm(const float* u, const float* gamma, const float* be
                              float* out32, uint16_t* outb, cudaStream_t st);
 
 // ---- attention (attention.cu)
-// head dim 64: tcgen05 kernel with 128-row q tiles and 3 length buckets (<= 128, <= 256,
-// <= 512 keys), each with its own work list; head dim 32: mma.sync, 64-row tiles, 1 list.
+// head dim 64: tcgen05 kernel with 128-row q tiles; head dim 32: mma.sync, 64-row tiles.
 inline int attn_tile_q(int head_dim) { return head_dim == 64 ? 128 : 64; }
-inline int attn_num_buckets(int tile_q) { return tile_q == 128 ? 3 : 1; }
-// upper bound on the number of q-tiles for T tokens in n requests (per bucket list)
+inline int attn_num_buckets(int) { return 1; }
+inline int64_t attn_bucket_capacity(int64_t, int) { return 0; }
+// upper bound on the number of q-tiles for T tokens in n requests
 inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q - 1) / tile_q + n; }
-inline int64_t attn_bucket_capacity(int64_t T, int n) { return attn_max_tiles(T, n, 128); }
-// grid bound of bucket b (tiles per request 1 / 2 / 4; requests at least 1 / 129 / 257 tokens)
-inline int64_t attn_bucket_grid(int64_t T, int n, int b) {
-  const int64_t minlen[3] = {1, 129, 257}, tiles[3] = {1, 2, 4};
-  const int64_t reqs = T / minlen[b] < n ? T / minlen[b] : n;
-  return reqs * tiles[b];
-}
 // total work-list entries to allocate for (T, n)
-inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) {
-  return tile_q == 128 ? 3 * attn_bucket_capacity(T, n) : attn_max_tiles(T, n, tile_q);
-}
+inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_max_tiles(T, n, tile_q); }
 // qkv [rows, 3H] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
 // work / num_work: attn_num_buckets(tile_q) lists of attn_bucket_capacity(T, n) entries
