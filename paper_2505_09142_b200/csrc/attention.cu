@@ -210,7 +210,7 @@ constexpr int kBlkBytes = TKB * TD * 2;  // 16 KB
 constexpr int kAttnTcSmem = 3 * kBlkBytes + 1024 + 256;
 constexpr uint32_t kOCol = 64;
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
     k_attention_tc(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ cu,
                    const int2* __restrict__ work, const int32_t* __restrict__ num_work, int H,
                    uint16_t* __restrict__ ctx, float scale_log2) {
@@ -290,17 +290,16 @@ __global__ void __launch_bounds__(128)
       tma_load_2d(sK, &tm, k_full, H + h * TD, start + (j + 1) * TKB);
     }
     const int nvalid_blk = L - j * TKB;  // keys >= L belong to other requests: masked
-    // pass A: block max (TMEM loads double-buffered)
-    uint32_t r[2][32];
+    // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM)
+    uint32_t r[32];
     float bm = -INFINITY;
-    tmem_ld_32x32b_x32(taddr, r[0]);
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < TKB / 32; ++c) {
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
-      if (c + 1 < TKB / 32) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        if (c * 32 + e < nvalid_blk) bm = fmaxf(bm, __uint_as_float(r[c & 1][e]));
+        if (c * 32 + e < nvalid_blk) bm = fmaxf(bm, __uint_as_float(r[e]));
     }
     const float m_new = fmaxf(m, bm * scale_log2);  // finite: every block has >= 1 valid key
     float alpha;
@@ -308,17 +307,16 @@ __global__ void __launch_bounds__(128)
     m = m_new;
     // pass B: p = exp2(s*scale - m), block sum, P (bf16 pairs) over consumed score columns
     float bl = 0.f;
-    tmem_ld_32x32b_x32(taddr, r[0]);
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < TKB / 32; ++c) {
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
-      if (c + 1 < TKB / 32) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
         float p0, p1;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[c & 1][e]), scale_log2, -m)));
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[c & 1][e + 1]), scale_log2, -m)));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[e]), scale_log2, -m)));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[e + 1]), scale_log2, -m)));
         p0 = (c * 32 + e < nvalid_blk) ? p0 : 0.f;
         p1 = (c * 32 + e + 1 < nvalid_blk) ? p1 : 0.f;
         bl += p0 + p1;
@@ -346,11 +344,13 @@ __global__ void __launch_bounds__(128)
       mbar_arrive_expect_tx(v_full, kBlkBytes);
       tma_load_2d(sV, &tm, v_full, 2 * H + h * TD, start + (j + 1) * TKB);
     }
-    tmem_ld_32x32b_x32(taddr + kOCol, r[0]);
-    tmem_ld_32x32b_x32(taddr + kOCol + 32, r[1]);
-    tc_wait_ld();
 #pragma unroll
-    for (int i = 0; i < TD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(r[i >> 5][i & 31]));
+    for (int hf = 0; hf < 2; ++hf) {
+      tmem_ld_32x32b_x32(taddr + kOCol + hf * 32, r);
+      tc_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[hf * 32 + i] = fmaf(o[hf * 32 + i], alpha, __uint_as_float(r[i]));
+    }
     tc_fence_before();
     __syncthreads();  // every row has read O_j before the next S MMA overwrites columns [0, 128)
   }
