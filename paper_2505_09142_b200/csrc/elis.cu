@@ -405,13 +405,9 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
               make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
               make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
               make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
+    ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
+         gemm_plan_set_ln(&L.p_ffn2, p->hb, L.ln2g, L.ln2b, cfg->ln_eps, T);
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    L.p_out.args.outb = L.p_ffn2.args.outb = p->hb;
-    L.p_out.args.gamma = L.ln1g;
-    L.p_out.args.beta = L.ln1b;
-    L.p_ffn2.args.gamma = L.ln2g;
-    L.p_ffn2.args.beta = L.ln2b;
-    L.p_out.args.eps = L.p_ffn2.args.eps = cfg->ln_eps;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "create sync");
 #undef ALLOC
@@ -702,12 +698,9 @@ elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* b
       K % 64 || N / gemm_block_n(N) > 4)
     return fail(ELIS_ERR_INVALID_ARG, "gemm_ln arguments");
   GemmPlan g;
-  if (!make_gemm_plan(&g, A, M, W, bias, resid_inout, resid_inout, M, N, K, EPI_BIAS_RESID_LN))
+  if (!make_gemm_plan(&g, A, M, W, bias, resid_inout, resid_inout, M, N, K, EPI_BIAS_RESID_LN) ||
+      !gemm_plan_set_ln(&g, outb, gamma, beta, eps, static_cast<uint64_t>(M)))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
-  g.args.outb = outb;
-  g.args.gamma = gamma;
-  g.args.beta = beta;
-  g.args.eps = eps;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -9,27 +9,29 @@
 // Design (sm_100a):
 //   * CTA pairs (tcgen05 cta_group::2): a 256 x BN output tile per pair; each CTA stages
 //     its 128 rows of A and half (BN/2 rows) of the B slab, the leader CTA issues
-//     tcgen05.mma M=256 for both, each CTA's TMEM holds its 128 accumulator rows.  Per
-//     CTA this halves the B bytes fetched per FLOP (the single-CTA 128 x 256 tile was L2
-//     bandwidth bound: 87 FLOP per L2 byte -> 131 with pairs);
+//     tcgen05.mma M=256 for both, each CTA's TMEM holds its 128 accumulator rows (per CTA
+//     this halves the B bytes fetched from L2 per FLOP);
 //   * persistent grid, static tile schedule; warp 0 = TMA producer (SWIZZLE_128B slabs,
 //     mbarrier ring, completion counted on the leader's barrier), warp 1 (leader) = the
-//     single-thread MMA issuer, warp 2 = TMEM allocator, warps 4..11 = epilogue (two
-//     warps per TMEM lane quarter, each owning half of the tile's columns);
+//     single-thread MMA issuer, warp 2 = TMEM allocator, warps 4..11 = epilogue (two warps
+//     per TMEM lane quarter, each owning half of the tile's columns);
 //   * two TMEM accumulators (2 x BN columns): the epilogue of tile i overlaps the mainloop
 //     of tile i+1;
-//   * ragged M handled by TMA out-of-bounds zero fill + masked stores (no padding of T);
+//   * epilogue global I/O goes through TMA in 32-row x 32-column boxes: the fp32 residual is
+//     TMA-loaded into per-warp swizzled slots (2-deep ring, issued before the accumulator is
+//     ready), results are staged in shared memory and written by TMA bulk stores.  (Thread =
+//     row stores would hit 32 cache lines per warp instruction.)  TMA also clips the ragged
+//     M tail, so T is never padded;
 //   * no split-K: every output row depends on its own A row only (batch invariance).
 //
 // EPI_BIAS_RESID_LN (attention-output and FFN2 + LayerNorm, rows a5+a6 / a8): a row of
 // H = 768 / 1024 columns spans CS = H / BN pairs, launched as one cluster of 2 x CS CTAs.
-// Each CTA adds bias + fp32 residual (prefetched by cp.async while the MMA runs), keeps v
-// in TMEM (tcgen05.st), computes per-row (mean, M2) over its columns and pushes them into
-// every peer's shared memory over DSMEM (st.shared::cluster + remote mbarrier arrive);
-// every CTA then merges the CS partials in rank order (Chan) and normalises its columns.
-// The fp32 residual stream is updated in place and the bf16 copy for the next GEMM is
-// written in the same pass: 10 B/element of epilogue traffic instead of 18 B with a
-// separate LayerNorm kernel.
+// Each CTA adds bias + residual, keeps v in TMEM (tcgen05.st), computes per-row (mean, M2)
+// over its columns and pushes them into every peer's shared memory over DSMEM
+// (st.shared::cluster + remote mbarrier arrive); every CTA then merges the CS partials in
+// rank order (Chan) and normalises its columns.  The fp32 residual stream is updated in
+// place and the bf16 copy for the next GEMM is written in the same pass: 10 B/element of
+// epilogue traffic instead of 18 B with a separate LayerNorm kernel.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -42,6 +44,7 @@ constexpr int BK = 64;
 constexpr int kEpiWarps = 8;
 constexpr int kGemmThreads = 128 + kEpiWarps * 32;  // 4 control warps + 8 epilogue warps
 constexpr int kMaxCluster = 4;                       // max N-tiles (pairs) per LN row
+constexpr int kBox = 32;                             // epilogue TMA boxes: 32 rows x 32 columns
 
 template <int BN>
 struct GemmCfg {
@@ -52,15 +55,25 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int CHUNKS_PER_WARP = BN / 64;   // 32-column chunks per epilogue warp
 };
-// Shared-memory plan.  RES (the epilogue reads an fp32 residual) trades operand stages for
-// a per-warp double-buffered residual staging area filled by cp.async ahead of use.
-template <int BN, bool RES>
+// Shared-memory plan per epilogue kind.
+template <int BN, int EPI>
 struct SmemPlan {
-  static constexpr int STAGES = RES ? 4 : 6;
-  static constexpr int RES_BYTES = RES ? kEpiWarps * 2 * 32 * 32 * 4 : 0;  // [warp][2][32 rows][32 f32]
+  static constexpr bool LN = EPI == EPI_BIAS_RESID_LN;
+  static constexpr bool RES = LN || EPI == EPI_BIAS_RESID_F32;
+  static constexpr bool OUT_F32 = RES;                 // f32 staging (4 KB per warp)
+  static constexpr bool OUT_BF16 = LN || !RES;         // bf16 staging (2 KB per warp)
+  static constexpr int NSTG = RES ? 1 : 2;             // staging buffers per warp
+  static constexpr int STAGES = RES ? 3 : 5;
+  static constexpr int RES_SLOT = kBox * kBox * 4;     // 4 KB fp32 residual box
+  static constexpr int RES_BYTES = RES ? kEpiWarps * 2 * RES_SLOT : 0;
+  static constexpr int STG_F32 = kBox * kBox * 4;      // 4 KB
+  static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
+  static constexpr int STG_WARP = NSTG * ((OUT_F32 ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
+  static constexpr int STG_BYTES = kEpiWarps * STG_WARP;
   // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta[256] f32
   static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 3 * 256 * 4;
-  static constexpr int SMEM_BYTES = STAGES * GemmCfg<BN>::STAGE_BYTES + RES_BYTES + AUX_BYTES + 1024;
+  static constexpr int SMEM_BYTES = STAGES * GemmCfg<BN>::STAGE_BYTES + RES_BYTES + STG_BYTES + AUX_BYTES + 1024;
+  static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
 
 // GELU(x) = x * Phi(x) (erf form).  Phi is evaluated as sigmoid(x * (c0 + c1 x^2 + c2 x^4))
@@ -90,32 +103,41 @@ ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, floa
   n_a = n;
 }
 
+// Byte offset of 16-byte piece k of row r in a 32-row box with 128-byte rows, SWIZZLE_128B.
+ELIS_DEV uint32_t sw128_off(int r, int k) { return static_cast<uint32_t>(r * 128 + ((k ^ (r & 7)) << 4)); }
+// Same for 64-byte rows, SWIZZLE_64B (16-byte pieces XOR bits [7,9) of the offset).
+ELIS_DEV uint32_t sw64_off(int r, int k) { return static_cast<uint32_t>(r * 64 + ((k ^ ((r >> 1) & 3)) << 4)); }
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
+              const __grid_constant__ CUtensorMap tmOb, const GemmArgs args) {
   using C = GemmCfg<BN>;
-  constexpr bool LN = (EPI == EPI_BIAS_RESID_LN);
-  constexpr bool RES = LN || (EPI == EPI_BIAS_RESID_F32);
-  using SP = SmemPlan<BN, RES>;
+  using SP = SmemPlan<BN, EPI>;
+  constexpr bool LN = SP::LN;
+  constexpr bool RES = SP::RES;
   constexpr int STAGES = SP::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C::A_BYTES;
-  float* res_base = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
-  uint8_t* aux = reinterpret_cast<uint8_t*>(res_base) + SP::RES_BYTES;
+  uint8_t* sRes = sB + STAGES * C::B_BYTES;   // [warp][2 slots][4 KB]
+  uint8_t* sStg = sRes + SP::RES_BYTES;       // [warp][NSTG][f32 4 KB | bf16 2 KB]
+  uint8_t* aux = sStg + SP::STG_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* sfull = tempty + 2;  // LN: stats slots filled by every CTA of the row group
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + 2);
-  float2* stats = reinterpret_cast<float2*>(aux + 512);   // [2][kMaxCluster][128]
-  float2* part = stats + 2 * kMaxCluster * 128;            // [2 halves][128]
-  float* sbias = reinterpret_cast<float*>(part + 2 * 128);  // [256]
-  float* sgam = sbias + 256;                                // [256]
-  float* sbet = sgam + 256;                                 // [256]
+  uint64_t* sfull = tempty + 2;    // LN: stats slots filled by every CTA of the row group
+  uint64_t* rfull = sfull + 2;     // [warp][2]: residual slot landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2 * kEpiWarps);
+  float2* stats = reinterpret_cast<float2*>(aux + 512);    // [2][kMaxCluster][128]
+  float2* part = stats + 2 * kMaxCluster * 128;             // [2 halves][128]
+  float* sbias = reinterpret_cast<float*>(part + 2 * 128);   // [256]
+  float* sgam = sbias + 256;                                 // [256]
+  float* sbet = sgam + 256;                                  // [256]
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -149,6 +171,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[a], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs (leader's copy used)
       mbar_init(&sfull[a], 4 * cpairs);      // one arrive per half-0 epilogue warp of every row peer
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&rfull[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -206,14 +229,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> global (each CTA: its 128 rows)
+    // ---------------- epilogue (each CTA: its 128 rows; warp: 32 rows x BN/2 columns)
     constexpr int CH = C::CHUNKS_PER_WARP;
     const int ew = warp - 4;             // 0..7
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int half = ew >> 2;            // which half of the tile's columns
     const int row_in_tile = q * 32 + lane;
     const int etid = ew * 32 + lane;     // 0..255
-    float* rbuf = res_base + ew * (2 * 32 * 32) + lane * 32;   // this thread's row in buffer 0
+    uint8_t* rslot = sRes + ew * 2 * SP::RES_SLOT;
+    uint64_t* rbar = rfull + 2 * ew;
+    uint8_t* stg = sStg + ew * SP::STG_WARP;
+    uint32_t rpar = 0;                   // parity bits of the two residual slots
+    int nstore = 0;                      // store groups issued by this warp
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), leader_rank);
     auto stage_vectors = [&](int n) {    // bias (+ gamma, beta) of tile columns -> shared memory
       if (etid < BN) {
@@ -224,33 +251,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     };
-    // residual chunk c of this thread's row -> buffer (c & 1), 16-byte pieces XOR-swizzled by row
-    auto prefetch_res = [&](int row, int col0, int c) {
-      const float* src = args.resid + static_cast<size_t>(row) * N + col0;
-      float* dst = rbuf + (c & 1) * (32 * 32);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) cp_async16(dst + ((k ^ (lane & 7)) * 4), src + 4 * k, true);
+    // residual box (32 rows x 32 columns at col0, row0) -> slot c & 1 (lane 0 issues)
+    auto load_res = [&](int row0, int col0, int c) {
+      if (lane == 0) {
+        fence_proxy_async_smem();   // slot previously read through the generic proxy
+        mbar_arrive_expect_tx(&rbar[c & 1], SP::RES_SLOT);
+        tma_load_2d(rslot + (c & 1) * SP::RES_SLOT, &tmR, &rbar[c & 1], col0, row0);
+      }
+    };
+    // staging buffer for the next store group (waits until its previous store read it)
+    auto next_stage = [&]() -> uint8_t* {
+      uint8_t* b = stg + (nstore % SP::NSTG) * (SP::STG_WARP / SP::NSTG);
+      if (lane == 0) tma_store_wait_read<SP::NSTG - 1>();
+      __syncwarp();
+      return b;
+    };
+    auto issue_store = [&](uint8_t* b, int row0, int col0) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (SP::OUT_F32) tma_store_2d(&tmO, b, col0, row0);
+        if constexpr (SP::OUT_BF16) {
+          if constexpr (SP::OUT_F32) tma_store_2d(&tmOb, b + SP::STG_F32, col0, row0);
+          else tma_store_2d(&tmO, b, col0, row0);
+        }
+        tma_store_commit();
+      }
+      ++nstore;
     };
     if constexpr (LN) {
       stage_vectors(pair_in_cluster);
       named_bar_sync(1, kEpiWarps * 32);
     }
     int it = 0;
+    bool res_prefetched = false;  // LN: the next tile's first residual boxes were issued early
     for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
       int m, n;
       tile_mn(t, m, n);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      const int row = m * 2 * BM + hrow * BM + row_in_tile;
-      const bool row_ok = row < M;
-      const int cbase = half * (BN / 2);  // first tile column of this warp
-      if constexpr (RES) {                // residual does not depend on the MMA: fetch it now
+      const int row0 = m * 2 * BM + hrow * BM + q * 32;   // first row of this warp's block
+      const int cbase = half * (BN / 2);                   // first tile column of this warp
+      if (RES && !res_prefetched) {       // residual does not depend on the MMA: fetch it now
 #pragma unroll
-        for (int c = 0; c < 2 && c < CH; ++c) {
-          if (row_ok) prefetch_res(row, n * BN + cbase + c * 32, c);
-          cp_async_commit();
-        }
+        for (int c = 0; c < 2 && c < CH; ++c) load_res(row0, n * BN + cbase + c * 32, c);
       }
+      res_prefetched = false;
       if constexpr (!LN) {
         named_bar_sync(1, kEpiWarps * 32);  // previous tile's readers of sbias are done
         stage_vectors(n);
@@ -278,24 +324,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           v[j + 3] = __uint_as_float(r[c & 1][j + 3]) + bb.w;
         }
         if constexpr (RES) {
-          if (c + 1 < CH) cp_async_wait<1>(); else cp_async_wait<0>();
-          if (row_ok) {
-            const float* src = rbuf + (c & 1) * (32 * 32);
+          const int s = c & 1;
+          mbar_wait(&rbar[s], (rpar >> s) & 1u);
+          rpar ^= 1u << s;
+          const uint8_t* src = rslot + s * SP::RES_SLOT;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float4 rr = *reinterpret_cast<const float4*>(src + ((k ^ (lane & 7)) * 4));
-              v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
-            }
-            if (c + 2 < CH) prefetch_res(row, col0 + 64, c + 2);
+          for (int k = 0; k < 8; ++k) {
+            const float4 rr = *reinterpret_cast<const float4*>(src + sw128_off(lane, k));
+            v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
           }
-          if (c + 2 < CH) cp_async_commit();
+          __syncwarp();  // every lane has read slot s
+          if (c + 2 < CH) load_res(row0, col0 + 64, c + 2);
         }
         if constexpr (LN) {
           // chunk statistics, merged into the running (n, mean, M2); v kept in TMEM
-          float s = 0.f;
+          float sum = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) s += v[j];
-          const float cm = s * (1.0f / 32.0f);
+          for (int j = 0; j < 32; ++j) sum += v[j];
+          const float cm = sum * (1.0f / 32.0f);
           float m2 = 0.f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) { const float d = v[j] - cm; m2 = fmaf(d, d, m2); }
@@ -305,26 +351,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
           tmem_st_32x32b_x32(taddr + c * 32, w);
-        } else if (row_ok) {
+        } else {
+          uint8_t* b = next_stage();
           if constexpr (EPI == EPI_BIAS_RESID_F32) {
-            float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(b + sw128_off(lane, k)) =
+                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           } else {
             if constexpr (EPI == EPI_BIAS_GELU_BF16) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
             }
-            uint4* o4 = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + static_cast<size_t>(row) * N + col0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              o4[j] = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                                 pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<uint4*>(b + sw64_off(lane, k)) =
+                  make_uint4(pack_bf16x2(v[8 * k + 0], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
+                             pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
           }
+          issue_store(b, row0, col0);
         }
       }
       if constexpr (LN) {
         tc_wait_st();
+        // pass 1 has consumed this tile's residual: start the next tile's first boxes now so the
+        // loads overlap the statistics exchange and pass 2
+        if (t + ncl < num_iter_tiles) {
+          int m2, n2;
+          tile_mn(t + ncl, m2, n2);
+          const int row0n = m2 * 2 * BM + hrow * BM + q * 32;
+#pragma unroll
+          for (int c = 0; c < 2 && c < CH; ++c) load_res(row0n, n2 * BN + cbase + c * 32, c);
+          res_prefetched = true;
+        }
         const int slot = it & 1;
         const uint32_t sph = (it >> 1) & 1;
         part[half * 128 + row_in_tile] = make_float2(st_mean, st_m2);
@@ -360,26 +419,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (c + 1 < CH) tmem_ld_32x32b_x32(taddr + (c + 1) * 32, r[(c + 1) & 1]);
           const int tcol = cbase + c * 32;
           const int col0 = n * BN + tcol;
-          if (row_ok) {
-            float y[32];
+          float y[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 g = *reinterpret_cast<const float4*>(sgam + tcol + j);
-              const float4 be = *reinterpret_cast<const float4*>(sbet + tcol + j);
-              y[j + 0] = (__uint_as_float(r[c & 1][j + 0]) - tmean) * rstd * g.x + be.x;
-              y[j + 1] = (__uint_as_float(r[c & 1][j + 1]) - tmean) * rstd * g.y + be.y;
-              y[j + 2] = (__uint_as_float(r[c & 1][j + 2]) - tmean) * rstd * g.z + be.z;
-              y[j + 3] = (__uint_as_float(r[c & 1][j + 3]) - tmean) * rstd * g.w + be.w;
-            }
-            float4* o4 = reinterpret_cast<float4*>(static_cast<float*>(args.out) + static_cast<size_t>(row) * N + col0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) o4[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
-            uint4* ob = reinterpret_cast<uint4*>(args.outb + static_cast<size_t>(row) * N + col0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              ob[j] = make_uint4(pack_bf16x2(y[8 * j + 0], y[8 * j + 1]), pack_bf16x2(y[8 * j + 2], y[8 * j + 3]),
-                                 pack_bf16x2(y[8 * j + 4], y[8 * j + 5]), pack_bf16x2(y[8 * j + 6], y[8 * j + 7]));
+          for (int j = 0; j < 32; j += 4) {
+            const float4 g = *reinterpret_cast<const float4*>(sgam + tcol + j);
+            const float4 be = *reinterpret_cast<const float4*>(sbet + tcol + j);
+            y[j + 0] = (__uint_as_float(r[c & 1][j + 0]) - tmean) * rstd * g.x + be.x;
+            y[j + 1] = (__uint_as_float(r[c & 1][j + 1]) - tmean) * rstd * g.y + be.y;
+            y[j + 2] = (__uint_as_float(r[c & 1][j + 2]) - tmean) * rstd * g.z + be.z;
+            y[j + 3] = (__uint_as_float(r[c & 1][j + 3]) - tmean) * rstd * g.w + be.w;
           }
+          uint8_t* b = next_stage();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<float4*>(b + sw128_off(lane, k)) =
+                make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+          uint8_t* bb = b + SP::STG_F32;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<uint4*>(bb + sw64_off(lane, k)) =
+                make_uint4(pack_bf16x2(y[8 * k + 0], y[8 * k + 1]), pack_bf16x2(y[8 * k + 2], y[8 * k + 3]),
+                           pack_bf16x2(y[8 * k + 4], y[8 * k + 5]), pack_bf16x2(y[8 * k + 6], y[8 * k + 7]));
+          issue_store(b, row0, col0);
         }
       }
       tc_fence_before();
@@ -387,6 +448,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // accumulator free: every lane's tcgen05.ld completed (wait::ld), so a relaxed arrive suffices
       if (lane == 0) mbar_arrive_remote_relaxed(tempty_leader + acc * 8);
     }
+    if (lane == 0) tma_store_wait_all<0>();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -398,7 +460,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 template <int BN, int EPI>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
-  using SP = SmemPlan<BN, EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID_F32>;
+  using SP = SmemPlan<BN, EPI>;
   auto kern = k_gemm_tc<BN, EPI>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -435,7 +497,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   const int work = ln ? num_m : num_m * num_n;
   const int ncl = work < max_clusters[csize] ? work : max_clusters[csize];
   cfg.gridDim = dim3(csize * ncl);
-  e = cudaLaunchKernelEx(&cfg, kern, g.tmA, g.tmB, g.args);
+  e = cudaLaunchKernelEx(&cfg, kern, g.tmA, g.tmB, g.tmR, g.tmO, g.tmOb, g.args);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -479,6 +541,19 @@ PFN_encodeTiled get_encode_fn() {
   }
   return fn;
 }
+
+bool make_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, uint32_t esize, const void* ptr, uint64_t rows,
+                  uint64_t cols, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * esize};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 }  // namespace
 
 bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
@@ -487,16 +562,8 @@ bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint6
 
 bool make_tmap_bf16_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
                         uint32_t box_rows) {
-  PFN_encodeTiled enc = get_encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  return make_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, box_cols, box_rows,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
@@ -513,7 +580,34 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
   g->args.out = out;
   if (!make_tmap_bf16_kmajor(&g->tmA, A, a_rows, K, BM)) return false;
   if (!make_tmap_bf16_kmajor(&g->tmB, W, N, K, gemm_block_n(N) / 2)) return false;
+  const bool res = epi == EPI_BIAS_RESID_F32 || epi == EPI_BIAS_RESID_LN;
+  // epilogue boxes: fp32 32 x 32 (128 B rows, SWIZZLE_128B); bf16 32 x 32 (64 B rows, SWIZZLE_64B)
+  if (res) {
+    if (!resid || !make_tmap_2d(&g->tmR, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, resid, a_rows, N, kBox, kBox,
+                                CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    if (!make_tmap_2d(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, a_rows, N, kBox, kBox,
+                      CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    g->tmOb = g->tmO;
+  } else {
+    if (!make_tmap_2d(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, a_rows, N, kBox, kBox,
+                      CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
+    g->tmR = g->tmO;
+    g->tmOb = g->tmO;
+  }
   return true;
+}
+
+bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const float* beta, float eps,
+                      uint64_t rows) {
+  g->args.outb = outb;
+  g->args.gamma = gamma;
+  g->args.beta = beta;
+  g->args.eps = eps;
+  return make_tmap_2d(&g->tmOb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, outb, rows, g->args.N, kBox, kBox,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 }  // namespace elis

@@ -24,11 +24,16 @@ struct GemmArgs {
   int M, N, K;
 };
 struct GemmPlan {
-  CUtensorMap tmA;
-  CUtensorMap tmB;
+  CUtensorMap tmA;   // A operand, bf16 K-major
+  CUtensorMap tmB;   // W operand, bf16 K-major
+  CUtensorMap tmR;   // residual f32 [rows, N], 32 x 32 boxes (RESID_F32 / RESID_LN)
+  CUtensorMap tmO;   // output: f32 32 x 32 boxes (RESID_F32 / RESID_LN) or bf16 32 x 32 boxes
+  CUtensorMap tmOb;  // RESID_LN: bf16 copy of the normalised rows, 32 x 32 boxes
   GemmArgs args;
   int epi;
 };
+// LN epilogue outputs: outb bf16 [rows, N], gamma/beta f32 [N]
+bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const float* beta, float eps, uint64_t rows);
 int gemm_block_n(int N);
 bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 // bf16 [rows, cols] row-major, box {box_cols (<= 64 for SWIZZLE_128B), box_rows}, SWIZZLE_128B
