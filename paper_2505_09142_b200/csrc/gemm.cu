@@ -55,17 +55,19 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int CHUNKS_PER_WARP = BN / 64;   // 32-column chunks per epilogue warp
 };
-// Shared-memory plan per epilogue kind.
-template <int BN, int EPI>
+// Shared-memory plan per epilogue kind.  DEEP (long-K residual GEMMs, e.g. FFN2: the mainloop
+// dominates) trades the second residual slot of each warp for a fourth operand stage.
+template <int BN, int EPI, bool DEEP>
 struct SmemPlan {
   static constexpr bool LN = EPI == EPI_BIAS_RESID_LN;
   static constexpr bool RES = LN || EPI == EPI_BIAS_RESID_F32;
   static constexpr bool OUT_F32 = RES;                 // f32 staging (4 KB per warp)
   static constexpr bool OUT_BF16 = LN || !RES;         // bf16 staging (2 KB per warp)
   static constexpr int NSTG = RES ? 1 : 2;             // staging buffers per warp
-  static constexpr int STAGES = RES ? 3 : 5;
+  static constexpr int NRES = (RES && DEEP) ? 1 : 2;   // residual slots per warp
+  static constexpr int STAGES = RES ? (DEEP ? 4 : 3) : 5;
   static constexpr int RES_SLOT = kBox * kBox * 4;     // 4 KB fp32 residual box
-  static constexpr int RES_BYTES = RES ? kEpiWarps * 2 * RES_SLOT : 0;
+  static constexpr int RES_BYTES = RES ? kEpiWarps * NRES * RES_SLOT : 0;
   static constexpr int STG_F32 = kBox * kBox * 4;      // 4 KB
   static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
   static constexpr int STG_WARP = NSTG * ((OUT_F32 ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
@@ -108,13 +110,14 @@ ELIS_DEV uint32_t sw128_off(int r, int k) { return static_cast<uint32_t>(r * 128
 // Same for 64-byte rows, SWIZZLE_64B (16-byte pieces XOR bits [7,9) of the offset).
 ELIS_DEV uint32_t sw64_off(int r, int k) { return static_cast<uint32_t>(r * 64 + ((k ^ ((r >> 1) & 3)) << 4)); }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool DEEP>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
               const __grid_constant__ CUtensorMap tmOb, const GemmArgs args) {
   using C = GemmCfg<BN>;
-  using SP = SmemPlan<BN, EPI>;
+  using SP = SmemPlan<BN, EPI, DEEP>;
+  constexpr int NRES = SP::NRES;
   constexpr bool LN = SP::LN;
   constexpr bool RES = SP::RES;
   constexpr int STAGES = SP::STAGES;
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int half = ew >> 2;            // which half of the tile's columns
     const int row_in_tile = q * 32 + lane;
     const int etid = ew * 32 + lane;     // 0..255
-    uint8_t* rslot = sRes + ew * 2 * SP::RES_SLOT;
+    uint8_t* rslot = sRes + ew * NRES * SP::RES_SLOT;
     uint64_t* rbar = rfull + 2 * ew;
     uint8_t* stg = sStg + ew * SP::STG_WARP;
     uint32_t rpar = 0;                   // parity bits of the two residual slots
@@ -255,8 +258,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto load_res = [&](int row0, int col0, int c) {
       if (lane == 0) {
         fence_proxy_async_smem();   // slot previously read through the generic proxy
-        mbar_arrive_expect_tx(&rbar[c & 1], SP::RES_SLOT);
-        tma_load_2d(rslot + (c & 1) * SP::RES_SLOT, &tmR, &rbar[c & 1], col0, row0);
+        mbar_arrive_expect_tx(&rbar[c % NRES], SP::RES_SLOT);
+        tma_load_2d(rslot + (c % NRES) * SP::RES_SLOT, &tmR, &rbar[c % NRES], col0, row0);
       }
     };
     // staging buffer for the next store group (waits until its previous store read it)
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int cbase = half * (BN / 2);                   // first tile column of this warp
       if (RES && !res_prefetched) {       // residual does not depend on the MMA: fetch it now
 #pragma unroll
-        for (int c = 0; c < 2 && c < CH; ++c) load_res(row0, n * BN + cbase + c * 32, c);
+        for (int c = 0; c < NRES && c < CH; ++c) load_res(row0, n * BN + cbase + c * 32, c);
       }
       res_prefetched = false;
       if constexpr (!LN) {
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           v[j + 3] = __uint_as_float(r[c & 1][j + 3]) + bb.w;
         }
         if constexpr (RES) {
-          const int s = c & 1;
+          const int s = c % NRES;
           mbar_wait(&rbar[s], (rpar >> s) & 1u);
           rpar ^= 1u << s;
           const uint8_t* src = rslot + s * SP::RES_SLOT;
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
           }
           __syncwarp();  // every lane has read slot s
-          if (c + 2 < CH) load_res(row0, col0 + 64, c + 2);
+          if (c + NRES < CH) load_res(row0, col0 + NRES * 32, c + NRES);
         }
         if constexpr (LN) {
           // chunk statistics, merged into the running (n, mean, M2); v kept in TMEM
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tile_mn(t + ncl, m2, n2);
           const int row0n = m2 * 2 * BM + hrow * BM + q * 32;
 #pragma unroll
-          for (int c = 0; c < 2 && c < CH; ++c) load_res(row0n, n2 * BN + cbase + c * 32, c);
+          for (int c = 0; c < NRES && c < CH; ++c) load_res(row0n, n2 * BN + cbase + c * 32, c);
           res_prefetched = true;
         }
         const int slot = it & 1;
@@ -458,10 +461,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool DEEP>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
-  using SP = SmemPlan<BN, EPI>;
-  auto kern = k_gemm_tc<BN, EPI>;
+  using SP = SmemPlan<BN, EPI, DEEP>;
+  auto kern = k_gemm_tc<BN, EPI, DEEP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
@@ -486,7 +489,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   // number of clusters that can be co-resident (one CTA per SM)
-  static int max_clusters[2 * kMaxCluster + 1] = {};
+  static int max_clusters[2 * kMaxCluster + 1] = {};  // per (BN, EPI, DEEP) instantiation
   if (max_clusters[csize] == 0) {
     cudaLaunchConfig_t q = cfg;
     q.gridDim = dim3(csize * (num_sms / csize));
@@ -509,18 +512,23 @@ int gemm_block_n(int N) { return (N % 256 == 0) ? 256 : 128; }
 cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
   if (g.args.M <= 0) return cudaSuccess;
   const bool b256 = gemm_block_n(g.args.N) == 256;
+  const bool deep = g.args.K >= 2048;  // long mainloop: a 4th operand stage beats a 2nd residual slot
   switch (g.epi) {
     case EPI_BIAS_BF16:
-      return b256 ? launch_bn<256, EPI_BIAS_BF16>(g, num_sms, st) : launch_bn<128, EPI_BIAS_BF16>(g, num_sms, st);
+      return b256 ? launch_bn<256, EPI_BIAS_BF16, false>(g, num_sms, st)
+                  : launch_bn<128, EPI_BIAS_BF16, false>(g, num_sms, st);
     case EPI_BIAS_GELU_BF16:
-      return b256 ? launch_bn<256, EPI_BIAS_GELU_BF16>(g, num_sms, st)
-                  : launch_bn<128, EPI_BIAS_GELU_BF16>(g, num_sms, st);
+      return b256 ? launch_bn<256, EPI_BIAS_GELU_BF16, false>(g, num_sms, st)
+                  : launch_bn<128, EPI_BIAS_GELU_BF16, false>(g, num_sms, st);
     case EPI_BIAS_RESID_F32:
-      return b256 ? launch_bn<256, EPI_BIAS_RESID_F32>(g, num_sms, st)
-                  : launch_bn<128, EPI_BIAS_RESID_F32>(g, num_sms, st);
+      return b256 ? launch_bn<256, EPI_BIAS_RESID_F32, false>(g, num_sms, st)
+                  : launch_bn<128, EPI_BIAS_RESID_F32, false>(g, num_sms, st);
     case EPI_BIAS_RESID_LN:
-      return b256 ? launch_bn<256, EPI_BIAS_RESID_LN>(g, num_sms, st)
-                  : launch_bn<128, EPI_BIAS_RESID_LN>(g, num_sms, st);
+      if (deep)
+        return b256 ? launch_bn<256, EPI_BIAS_RESID_LN, true>(g, num_sms, st)
+                    : launch_bn<128, EPI_BIAS_RESID_LN, true>(g, num_sms, st);
+      return b256 ? launch_bn<256, EPI_BIAS_RESID_LN, false>(g, num_sms, st)
+                  : launch_bn<128, EPI_BIAS_RESID_LN, false>(g, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }
