@@ -290,11 +290,15 @@ __global__ void __launch_bounds__(128, 4)
       tma_load_2d(sK, &tm, k_full, H + h * TD, start + (j + 1) * TKB);
     }
     const int nvalid_blk = L - j * TKB;  // keys >= L belong to other requests: masked
+    // 32-key chunks holding valid keys; warps whose 32 query rows all lie beyond L skip the
+    // softmax (their rows are never stored; MMA rows are independent)
+    const int nch = min(TKB / 32, (nvalid_blk + 31) / 32);
+    const bool warp_active = q0 + warp * 32 < L;
     // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM)
     uint32_t r[32];
     float bm = -INFINITY;
 #pragma unroll 1
-    for (int c = 0; c < TKB / 32; ++c) {
+    for (int c = 0; c < (warp_active ? nch : 0); ++c) {
       tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
 #pragma unroll
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(128, 4)
     // pass B: p = exp2(s*scale - m), block sum, P (bf16 pairs) over consumed score columns
     float bl = 0.f;
 #pragma unroll 1
-    for (int c = 0; c < TKB / 32; ++c) {
+    for (int c = 0; c < (warp_active ? nch : 0); ++c) {
       tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
       uint32_t pk[16];
@@ -331,8 +335,8 @@ __global__ void __launch_bounds__(128, 4)
     if (issuer) {
       tc_fence_after();
       mbar_wait(v_full, ph);
-#pragma unroll
-      for (int ks = 0; ks < TKB / 16; ++ks) {
+      const int nks = min(TKB / 16, (nvalid_blk + 15) / 16);  // 16-key steps holding valid keys
+      for (int ks = 0; ks < nks; ++ks) {
         const uint64_t dv = make_sw128_desc(smem_u32(sV + ks * (16 * TD * 2)));
         tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, ks > 0);
       }
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(128, 4)
       tma_load_2d(sV, &tm, v_full, 2 * H + h * TD, start + (j + 1) * TKB);
     }
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
+    for (int hf = 0; hf < (warp_active ? 2 : 0); ++hf) {
       tmem_ld_32x32b_x32(taddr + kOCol + hf * 32, r);
       tc_wait_ld();
 #pragma unroll
