@@ -257,6 +257,49 @@ def random_predictions(n: int, seed: int = 0, kind: str = "mixed") -> np.ndarray
     return v.astype(np.float32)
 
 
+# ----------------------------------------------------------------------------- request streams
+
+# Average LLM latencies over 500 prompts on A100 (ms), PAPER.md tab:ml-models.
+MODEL_AVG_LATENCY_MS = {"opt6.7": 1315.5, "opt13": 2643.2, "lam7": 6522.2, "lam13": 8610.2, "vic": 2964.9}
+GAMMA_ALPHA, GAMMA_BETA_S = 0.73, 10.41  # FabriX inter-arrival fit
+
+
+def average_request_rate(avg_latency_ms: float, batch_size: int) -> float:
+    """Requests/s that keep a backend of `batch_size` busy: (1000 / avg latency) x batch size
+    (P:481, P:492 -- the formula's braces are garbled in the source; R17)."""
+    return 1000.0 / avg_latency_ms * batch_size
+
+
+def arrival_times_ms(n: int, rate_per_s: float, alpha: float = 1.0, seed: int = 0) -> np.ndarray:
+    """Cumulative arrival times (ms) with Gamma(alpha, 1 / (alpha * rate)) inter-arrivals:
+    alpha = 1 is a Poisson process (BASELINE.json configs[3]); alpha = 0.73 is the FabriX shape
+     rescaled to the requested mean rate."""
+    rng = _rng(SUB_ARRIVALS, 7000 + seed)
+    gaps_s = rng.gamma(alpha, 1.0 / (alpha * rate_per_s), n)
+    return np.cumsum(gaps_s) * 1000.0
+
+
+def stream_requests(n: int, seed: int = 0):
+    """n synthetic requests: prompt token ids ([CLS] + prompt + [SEP]) and true total output
+    lengths (trace-shaped: prompt ~ LogNormal(ln 48, 1), response ~ LogNormal(ln 180, 0.8)).
+    Returns (list of int32 prompt arrays, int32 total outputs)."""
+    rng = _rng(SUB_OUTPUTS, seed)
+    p = np.clip(np.rint(rng.lognormal(np.log(48.0), 1.0, n)), 4, 384).astype(np.int64)
+    r = np.clip(np.rint(rng.lognormal(np.log(180.0), 0.8, n)), 1, 1536).astype(np.int32)
+    prompts = []
+    for i in range(n):
+        t = rng.integers(1000, VOCAB, p[i] + 2).astype(np.int32)
+        t[0], t[-1] = CLS_ID, SEP_ID
+        prompts.append(t)
+    return prompts, r
+
+
+def response_tokens(job_id: int, total: int, seed: int = 0) -> np.ndarray:
+    """The (synthetic) tokens the served LLM generates for job `job_id`."""
+    rng = _rng(SUB_OUTPUTS, 100000 + seed, job_id)
+    return rng.integers(1000, VOCAB, total).astype(np.int32)
+
+
 def random_sched_state(n: int, seed: int = 0, frac_running: float = 0.05, frac_empty: float = 0.05):
     """generated (int32, <0 = empty slot), order (unique uint32 rank of (arrival, id)),
     running (uint8) for select tests."""

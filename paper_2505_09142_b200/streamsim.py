@@ -1,0 +1,169 @@
+"""Closed-loop ISRTF iteration driver + stream simulator (
+BASELINE.json configs[3]: Poisson arrivals, ISRTF with preemption vs FCFS, predictor on GPU).
+
+It runs PAPER.md Algorithm 1 (alg:scheduler_flow) for one backend worker with the
+GPU hot path in the loop.  At every window boundary:
+  * the due set -- new arrivals and the jobs that just ran a window (lines 10-18; jobs waiting
+    in the Priority Buffer keep their cached priority, R8) -- is re-predicted by
+    elis_predict_remaining straight into a device-resident in-flight table (out_slot);
+  * elis_isrtf_select picks the next batch over the whole table (line 19) with the
+    running flags of the previous batch (preemption);
+  * the backend is modelled as windows of K = 50 tokens ending early when a member finishes
+    (P:341-342), lasting TTFT (first execution) + TPOT x tokens (Sec. 2.1).
+The LLM itself is out of scope: each job's response tokens are synthetic and
+its true length is known to the simulator only.
+
+Priority sources: "gpu" (the BGE + 8-FC predictor; random-init weights carry no length
+signal, so this measures the mechanics and the per-iteration GPU overhead), "oracle" (true
+remaining tokens: the SRTF bound, written into the table) and policy FCFS.
+
+Every GPU decision is recorded so tests can replay the run through the fp64 oracle simulator
+and require identical schedules.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import binding, inputs
+
+POLICY_ISRTF, POLICY_FCFS = binding.POLICY_ISRTF, binding.POLICY_FCFS
+
+
+@dataclass
+class StreamResult:
+    first: np.ndarray                 # first-execution time per job (ms)
+    finish: np.ndarray                # completion time per job (ms)
+    arrival: np.ndarray
+    iterations: int
+    gpu_ms_per_iter: float            # device-side predict + select time per window (CUDA events)
+    host_ms_per_iter: float           # wall clock of the whole driver step per window
+    predicted_per_iter: float         # mean due-set size
+    recorded: dict = field(default_factory=dict)  # (job, generated) -> fp32 priority used
+
+    @property
+    def jct(self) -> np.ndarray:
+        return self.finish - self.arrival
+
+    def summary(self) -> dict:
+        return {"mean_jct_ms": float(self.jct.mean()), "mean_queue_ms": float((self.first - self.arrival).mean()),
+                "iterations": self.iterations, "gpu_ms_per_iter": self.gpu_ms_per_iter,
+                "host_ms_per_iter": self.host_ms_per_iter, "due_per_iter": self.predicted_per_iter}
+
+
+def build_sequence(prompt: np.ndarray, response: np.ndarray, generated: int, max_len: int = 512) -> np.ndarray:
+    """'the prompt attached with the answer': [CLS] prompt [SEP] + the response so far.
+    Longer than max_len: keep the most recent <= 254 response tokens and the head of the prompt
+    (R7)."""
+    resp = response[:generated]
+    if prompt.size + resp.size <= max_len:
+        return np.concatenate([prompt, resp]).astype(np.int32)
+    keep_resp = min(resp.size, 254)
+    head = prompt[:max_len - keep_resp]
+    return np.concatenate([head, resp[resp.size - keep_resp:]]).astype(np.int32)
+
+
+class StreamSim:
+    def __init__(self, predictor: binding.Predictor | None, policy: int = POLICY_ISRTF, cap: int = 4,
+                 window: int = inputs.WINDOW_K, ttft_ms: float = 0.0, tpot_ms: float = 1.0,
+                 allow_preempt: bool = True, priority: str = "gpu", seed: int = 0):
+        if priority == "gpu" and predictor is None and policy == POLICY_ISRTF:
+            raise ValueError("priority='gpu' needs a predictor")
+        self.P = predictor
+        self.policy, self.cap, self.K = policy, cap, window
+        self.ttft, self.tpot, self.allow = ttft_ms, tpot_ms, allow_preempt
+        self.priority, self.seed = priority, seed
+
+    def run(self, prompts, totals, arrivals_ms, select_predictor: binding.Predictor | None = None) -> StreamResult:
+        import torch
+        P = self.P if self.P is not None else select_predictor
+        if P is None:
+            raise ValueError("a predictor (for the device select) is required")
+        nj = len(prompts)
+        order = np.argsort(arrivals_ms, kind="stable")
+        assert (order == np.arange(nj)).all(), "jobs must be sorted by arrival (id = arrival rank)"
+        responses = [inputs.response_tokens(j, int(totals[j]), self.seed) for j in range(nj)]
+        gen = np.full(nj, -1, np.int32)            # -1: not arrived or finished (ineligible slot)
+        first = np.full(nj, np.nan)
+        finish = np.full(nj, np.nan)
+        running = np.zeros(nj, np.uint8)
+        started = np.zeros(nj, bool)
+        dev = torch.device("cuda")
+        st = torch.cuda.current_stream()
+        d_table = torch.zeros(nj, device=dev)
+        d_gen = torch.empty(nj, dtype=torch.int32, device=dev)
+        d_run = torch.empty(nj, dtype=torch.uint8, device=dev)
+        d_order = torch.arange(nj, dtype=torch.int32, device=dev).to(torch.int32)
+        d_ids = torch.empty(self.cap, dtype=torch.int32, device=dev)
+        d_cnt = torch.empty(1, dtype=torch.int32, device=dev)
+        h_ids = torch.empty(self.cap, dtype=torch.int32).pin_memory()
+        h_cnt = torch.empty(1, dtype=torch.int32).pin_memory()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        recorded = {}
+        t = 0.0
+        nxt = 0                                     # next job to arrive
+        due: list[int] = []
+        iters, gpu_ms, host_ms, due_total = 0, 0.0, 0.0, 0
+        done = 0
+        while done < nj:
+            while nxt < nj and arrivals_ms[nxt] <= t:
+                gen[nxt] = 0
+                due.append(nxt)
+                nxt += 1
+            if not (gen >= 0).any():
+                t = float(arrivals_ms[nxt])
+                running[:] = 0
+                continue
+            h0 = time.perf_counter()
+            ev0.record(st)
+            if due and self.policy == POLICY_ISRTF:
+                if self.priority == "gpu":
+                    seqs = [build_sequence(prompts[j], responses[j], int(gen[j])) for j in due]
+                    lens = np.array([s.size for s in seqs], np.int32)
+                    toks = torch.from_numpy(np.concatenate(seqs)).to(dev, non_blocking=True)
+                    slots = torch.from_numpy(np.array(due, np.int32)).to(dev, non_blocking=True)
+                    P.predict_remaining(toks, torch.from_numpy(lens).to(dev, non_blocking=True), int(lens.sum()),
+                                        d_table, out_slot=slots, stream=st)
+                else:  # "oracle": true remaining tokens (SRTF bound)
+                    rem = (totals[due] - gen[due]).astype(np.float32)
+                    d_table[torch.from_numpy(np.array(due, np.int64)).to(dev)] = torch.from_numpy(rem).to(dev)
+            d_gen.copy_(torch.from_numpy(gen), non_blocking=True)
+            d_run.copy_(torch.from_numpy(running), non_blocking=True)
+            P.isrtf_select(d_table, d_gen, self.cap, d_ids, policy=self.policy, allow_preempt=self.allow,
+                           order=d_order, running=d_run, out_count=d_cnt, stream=st)
+            h_ids.copy_(d_ids, non_blocking=True)
+            h_cnt.copy_(d_cnt, non_blocking=True)
+            ev1.record(st)
+            st.synchronize()
+            gpu_ms += ev0.elapsed_time(ev1)
+            if due and self.policy == POLICY_ISRTF:
+                vals = d_table[torch.from_numpy(np.array(due, np.int64)).to(dev)].cpu().numpy()
+                for j, v in zip(due, vals):
+                    recorded[(int(j), int(gen[j]))] = float(v)
+            due_total += len(due)
+            batch = [int(x) for x in h_ids.numpy()[:int(h_cnt.item())]]
+            assert batch, "select returned an empty batch with eligible jobs"
+            w = min(self.K, min(int(totals[j] - gen[j]) for j in batch))
+            dur = (self.ttft if any(not started[j] for j in batch) else 0.0) + self.tpot * w
+            for j in batch:
+                if not started[j]:
+                    started[j] = True
+                    first[j] = t
+            t += dur
+            running[:] = 0
+            due = []
+            for j in batch:
+                gen[j] += w
+                if gen[j] >= totals[j]:
+                    finish[j] = t
+                    gen[j] = -1
+                    done += 1
+                else:
+                    running[j] = 1
+                    due.append(j)
+            iters += 1
+            host_ms += (time.perf_counter() - h0) * 1e3
+        return StreamResult(first, finish, np.asarray(arrivals_ms, float), iters, gpu_ms / max(iters, 1),
+                            host_ms / max(iters, 1), due_total / max(iters, 1), recorded)

@@ -1,0 +1,66 @@
+"""Closed-loop stream simulator with the GPU hot path in the loop (SURVEY.md f1,
+BASELINE.json configs[3]) replayed through the fp64 oracle simulator: given the same
+priorities, every scheduling decision -- hence every first-execution and finish time -- must be
+identical (bit-exact selects + the same window rules, Alg. 1)."""
+import numpy as np
+import pytest
+
+from paper_2505_09142_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tiny_predictor(cuda_lib):
+    from paper_2505_09142_b200 import binding
+    cfg = inputs.CONFIGS["tiny"]
+    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg, seed=0)), 64 * 512, 64)
+    yield P
+    P.close()
+
+
+def make_stream(n, mult, seed):
+    prompts, totals = inputs.stream_requests(n, seed=seed)
+    totals = np.minimum(totals, 400)   # keep the test short
+    tpot = 0.95 * inputs.MODEL_AVG_LATENCY_MS["lam13"] / float(totals.mean())
+    rate = mult * inputs.average_request_rate(inputs.MODEL_AVG_LATENCY_MS["lam13"], 4)
+    arr = inputs.arrival_times_ms(n, rate, alpha=1.0, seed=seed)
+    return prompts, totals, arr, 0.05 * inputs.MODEL_AVG_LATENCY_MS["lam13"], tpot
+
+
+def replay(totals, arr, policy, cap, ttft, tpot, allow, priority):
+    from oracle import sim
+    jobs = [sim.SimJob(i, float(arr[i]), int(totals[i])) for i in range(len(totals))]
+    r = sim.simulate(jobs, policy, cap=cap, K=50, ttft=ttft, tpot=tpot, allow_preempt=allow, priority=priority)
+    return np.array([r[i][0] for i in range(len(jobs))]), np.array([r[i][1] for i in range(len(jobs))])
+
+
+@pytest.mark.parametrize("source,policy,allow", [("gpu", 0, True), ("oracle", 0, True), ("gpu", 0, False),
+                                                 ("none", 1, True)])
+def test_stream_sim_matches_oracle_replay(tiny_predictor, source, policy, allow):
+    from oracle import sim
+    from paper_2505_09142_b200.streamsim import StreamSim
+    prompts, totals, arr, ttft, tpot = make_stream(120, 3.0, seed=1)
+    S = StreamSim(tiny_predictor, policy=policy, cap=4, ttft_ms=ttft, tpot_ms=tpot, allow_preempt=allow,
+                  priority=source if source != "none" else "gpu")
+    res = S.run(prompts, totals, arr)
+    assert np.isfinite(res.finish).all() and (res.finish >= res.first).all()
+    if source == "gpu" and policy == 0:
+        prio = lambda job, g: res.recorded[(job.id, g)]
+    else:
+        prio = sim.oracle_remaining
+    first, finish = replay(totals, arr, policy, 4, ttft, tpot, allow, prio)
+    np.testing.assert_array_equal(res.first, first)
+    np.testing.assert_array_equal(res.finish, finish)
+
+
+def test_srtf_beats_fcfs_on_the_stream(tiny_predictor):
+    """With true remaining as priority (SRTF bound) mean JCT is below FCFS."""
+    from paper_2505_09142_b200.streamsim import StreamSim
+    prompts, totals, arr, ttft, tpot = make_stream(150, 5.0, seed=2)
+    f = StreamSim(tiny_predictor, policy=1, cap=4, ttft_ms=ttft, tpot_ms=tpot).run(prompts, totals, arr)
+    s = StreamSim(tiny_predictor, policy=0, cap=4, ttft_ms=ttft, tpot_ms=tpot, priority="oracle").run(
+        prompts, totals, arr)
+    assert s.jct.mean() < f.jct.mean()
