@@ -294,16 +294,29 @@ __global__ void __launch_bounds__(128, 4)
     // softmax (their rows are never stored; MMA rows are independent)
     const int nch = min(TKB / 32, (nvalid_blk + 31) / 32);
     const bool warp_active = q0 + warp * 32 < L;
-    // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM)
+    // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM).
+    // Only the chunk holding the last valid key is masked; full chunks take a plain max tree.
     uint32_t r[32];
     float bm = -INFINITY;
 #pragma unroll 1
     for (int c = 0; c < (warp_active ? nch : 0); ++c) {
       tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
+      const int nv = nvalid_blk - c * 32;
+      if (nv >= 32) {
+        float t[16];
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (c * 32 + e < nvalid_blk) bm = fmaxf(bm, __uint_as_float(r[e]));
+        for (int e = 0; e < 16; ++e) t[e] = fmaxf(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+          for (int e = 0; e < w; ++e) t[e] = fmaxf(t[e], t[e + w]);
+        bm = fmaxf(bm, t[0]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < nv) bm = fmaxf(bm, __uint_as_float(r[e]));
+      }
     }
     const float m_new = fmaxf(m, bm * scale_log2);  // finite: every block has >= 1 valid key
     float alpha;
@@ -315,17 +328,22 @@ __global__ void __launch_bounds__(128, 4)
     for (int c = 0; c < (warp_active ? nch : 0); ++c) {
       tmem_ld_32x32b_x32(taddr + c * 32, r);
       tc_wait_ld();
+      const int nv = nvalid_blk - c * 32;
+      float p[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p[e]) : "f"(fmaf(__uint_as_float(r[e]), scale_log2, -m)));
+      if (nv < 32) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) p[e] = (e < nv) ? p[e] : 0.f;
+      }
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial sums, fixed order
+#pragma unroll
+      for (int e = 0; e < 32; ++e) sacc[e & 3] += p[e];
+      bl += (sacc[0] + sacc[1]) + (sacc[2] + sacc[3]);
       uint32_t pk[16];
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        float p0, p1;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(__uint_as_float(r[e]), scale_log2, -m)));
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(__uint_as_float(r[e + 1]), scale_log2, -m)));
-        p0 = (c * 32 + e < nvalid_blk) ? p0 : 0.f;
-        p1 = (c * 32 + e + 1 < nvalid_blk) ? p1 : 0.f;
-        bl += p0 + p1;
-        pk[e / 2] = pack_bf16x2(p0, p1);
-      }
+      for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
       tmem_st_32x32b_x16(taddr + c * 16, pk);
     }
     l = l * alpha + bl;
