@@ -34,7 +34,9 @@ elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* b
                             int32_t K, void* stream);
 
 /* Varlen bidirectional multi-head attention ("process tokens in parallel").
- * qkv bf16 [T, 3H] (Q | K | V, head h at columns h*d .. h*d+d-1 of each third),
+ * d = 64: qkv bf16 head-major planes [3 * num_heads][T][64] (plane h = Q of head h, plane
+ *         num_heads + h = K, plane 2 num_heads + h = V) -- the layout the QKV GEMM writes;
+ * d = 32: qkv bf16 [T, 3H] (Q | K | V, head h at columns h*d .. h*d+d-1 of each third).
  * lengths int32 [n] (sum == T, each in [1, 512]); ctx bf16 [T, H] = per request i and head h:
  * softmax(Q_h K_h^T / sqrt(d)) V_h over the request's own L_i tokens.  d = H / num_heads in {32, 64}. */
 elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T,

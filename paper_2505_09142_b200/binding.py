@@ -232,7 +232,7 @@ def op_gemm_ln(A, W, bias, resid_inout, gamma, beta, eps: float, outb, stream=No
 
 
 def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None):
-    check(lib().elis_op_attention(_ptr(qkv), _ptr(lengths), int(lengths.shape[0]), int(qkv.shape[0]), hidden,
+    check(lib().elis_op_attention(_ptr(qkv), _ptr(lengths), int(lengths.shape[0]), int(ctx.shape[0]), hidden,
                                   num_heads, _ptr(ctx), _stream(stream)), "elis_op_attention")
 
 

@@ -233,7 +233,7 @@ ELIS_DEV AttnItem attn_item(int item, int nh, const int32_t* __restrict__ cu, co
 __global__ void __launch_bounds__(kAttnThreads, kAttnCtasPerSm)
     k_attention_tc(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ cu,
                    const int2* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
-                   uint16_t* __restrict__ ctx, float scale_log2) {
+                   uint16_t* __restrict__ ctx, float scale_log2, int Tp) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -282,15 +282,15 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnCtasPerSm)
         const int qs = qn & 1;
         mbar_wait(&q_empty[qs], ((qn >> 1) & 1) ^ 1u);
         mbar_arrive_expect_tx(&q_full[qs], kBlkBytes);
-        tma_load_2d(sQ + qs * kBlkBytes, &tm, &q_full[qs], it.h * TD, it.start + it.q0);
+        tma_load_2d(sQ + qs * kBlkBytes, &tm, &q_full[qs], 0, it.h * Tp + it.start + it.q0);
         ++qn;
         for (int j = 0; j < it.nkb; ++j, ++kvn) {
           const int s = kvn & 1;
           mbar_wait(&kv_empty[s], ((kvn >> 1) & 1) ^ 1u);
           mbar_arrive_expect_tx(&kv_full[s], 2 * kBlkBytes);
           uint8_t* slot = sKV + s * 2 * kBlkBytes;
-          tma_load_2d(slot, &tm, &kv_full[s], H + it.h * TD, it.start + j * TKB);
-          tma_load_2d(slot + kBlkBytes, &tm, &kv_full[s], 2 * H + it.h * TD, it.start + j * TKB);
+          tma_load_2d(slot, &tm, &kv_full[s], 0, (nh + it.h) * Tp + it.start + j * TKB);
+          tma_load_2d(slot + kBlkBytes, &tm, &kv_full[s], 0, (2 * nh + it.h) * Tp + it.start + j * TKB);
         }
       }
     }
@@ -470,12 +470,14 @@ __global__ void __launch_bounds__(kAttnThreads, kAttnCtasPerSm)
 
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
   // 64 bf16 = 128 B inner box (one SWIZZLE_128B row), 128 rows
-  return make_tmap_bf16_box(m, qkv, rows, static_cast<uint64_t>(3 * H), 64, 128);
+  // head-major planes [3 * nh][rows][64] viewed as one [3 * nh * rows, 64] matrix: 128-token boxes of one
+  // head's Q, K or V are contiguous 16 KB blocks (64 bf16 = one SWIZZLE_128B row)
+  return make_tmap_bf16_box(m, qkv, rows * static_cast<uint64_t>(3 * (H / 64)), 64, 64, 128);
 }
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const int2* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             uint16_t* ctx, cudaStream_t st) {
+                             int64_t plane_rows, uint16_t* ctx, cudaStream_t st) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
@@ -495,7 +497,7 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
     const int64_t items = max_tiles * num_heads;
     const int g = static_cast<int>(items < kAttnCtasPerSm * num_sms ? items : kAttnCtasPerSm * num_sms);
     k_attention_tc<<<g, kAttnThreads, kAttnTcSmem, st>>>(*tm_qkv, cu_seqlens, work, num_work, H, num_heads, ctx,
-                                                         scale_log2);
+                                                         scale_log2, static_cast<int>(plane_rows));
   } else if (d == 32) {
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
   } else {

@@ -96,6 +96,12 @@ ELIS_DEV void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0, i
                "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
                : "memory");
 }
+ELIS_DEV void tma_store_3d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 ELIS_DEV void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the shared-memory source of all but the N most recent store groups has been read
 template <int N>

@@ -405,6 +405,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
               make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
               make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
               make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
+    // head dim 64: QKV written head-major ([3 nh][T][64]) for the tcgen05 attention's TMA boxes
+    if (H / cfg->num_heads == 64) ok = ok && gemm_plan_set_head_major(&L.p_qkv, p->qkv, T);
     ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
          gemm_plan_set_ln(&L.p_ffn2, p->hb, L.ln2g, L.ln2b, cfg->ln_eps, T);
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -428,6 +430,7 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   const elis_config& c = p->cfg;
   const int H = c.hidden;
   const int M = static_cast<int>(total_tokens);
+  const int64_t T_cap = c.max_tokens;  // rows of each head-major qkv plane
   p->last_stream = st;
   p->last_T = total_tokens;
 
@@ -441,7 +444,7 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     LAUNCH(p, PC_ATTN, st,
-           launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, p->ctx,
+           launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
                             st));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
@@ -729,7 +732,7 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(int2)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, ctx, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);

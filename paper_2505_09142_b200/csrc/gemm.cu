@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if constexpr (SP::OUT_F32) tma_store_2d(&tmO, b, col0, row0);
         if constexpr (SP::OUT_BF16) {
           if constexpr (SP::OUT_F32) tma_store_2d(&tmOb, b + SP::STG_F32, col0, row0);
+          else if (args.out_head_major) tma_store_3d(&tmO, b, col0 & 63, row0, col0 >> 6);
           else tma_store_2d(&tmO, b, col0, row0);
         }
         tma_store_commit();
@@ -606,6 +607,23 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
     g->tmOb = g->tmO;
   }
   return true;
+}
+
+bool gemm_plan_set_head_major(GemmPlan* g, void* out, uint64_t rows) {
+  if (g->epi != EPI_BIAS_BF16 || g->args.N % 64 != 0) return false;
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  // [planes = N/64][rows][64] bf16; box 32 columns x 32 rows x 1 plane, 64-byte rows (SWIZZLE_64B)
+  cuuint64_t dims[3] = {64, rows, static_cast<cuuint64_t>(g->args.N / 64)};
+  cuuint64_t strides[2] = {64 * 2, rows * 64 * 2};
+  cuuint32_t box[3] = {kBox, kBox, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, out, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  g->args.out = out;
+  g->args.out_head_major = 1;
+  return r == CUDA_SUCCESS;
 }
 
 bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const float* beta, float eps,

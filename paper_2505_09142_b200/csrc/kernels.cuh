@@ -22,6 +22,7 @@ struct GemmArgs {
   const float* beta;    // RESID_LN
   float eps;
   int M, N, K;
+  int out_head_major;   // bf16 output written as [N/64 planes][rows][64] (attention-friendly qkv)
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major
@@ -32,6 +33,9 @@ struct GemmPlan {
   GemmArgs args;
   int epi;
 };
+// bf16 output in head-major planes: out[N/64][rows][64] (the QKV projection feeding attention:
+// every (head, 128-token) box of Q, K or V is one contiguous 16 KB block)
+bool gemm_plan_set_head_major(GemmPlan* g, void* out, uint64_t rows);
 // LN epilogue outputs: outb bf16 [rows, N], gamma/beta f32 [N]
 bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const float* beta, float eps, uint64_t rows);
 int gemm_block_n(int N);
@@ -65,12 +69,13 @@ inline int64_t attn_bucket_capacity(int64_t, int) { return 0; }
 inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q - 1) / tile_q + n; }
 // total work-list entries to allocate for (T, n)
 inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_max_tiles(T, n, tile_q); }
-// qkv [rows, 3H] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
+// head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
 // work / num_work: attn_num_buckets(tile_q) lists of attn_bucket_capacity(T, n) entries
+// head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H]
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const int2* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             uint16_t* ctx, cudaStream_t st);
+                             int64_t plane_rows, uint16_t* ctx, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,

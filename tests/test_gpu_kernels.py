@@ -27,6 +27,16 @@ def to_np(t):
     return t.detach().float().cpu().numpy().astype(np.float64)
 
 
+def attn_layout(qkv, H, nh):
+    """qkv [T, 3H] -> the layout elis_op_attention expects: head-major planes [3 nh][T][64] for
+    d = 64 (what the QKV GEMM writes), unchanged [T, 3H] for d = 32."""
+    d = H // nh
+    if d != 64:
+        return qkv
+    T = qkv.shape[0]
+    return qkv.view(T, 3, nh, d).permute(1, 2, 0, 3).contiguous()
+
+
 @pytest.mark.parametrize("M", [1, 129, 300, 1000])
 @pytest.mark.parametrize("N,K", [(384, 128), (128, 128), (512, 128), (2304, 768), (768, 768), (3072, 768),
                                  (768, 3072), (1024, 1024)])
@@ -74,7 +84,7 @@ def test_attention_varlen_parity(cuda_lib, d, nh):
     qkv, qkv64 = bf16_tensor(rng.normal(0, 1.0, (T, 3 * H)))
     ctx = torch.full((T, H), float("nan"), dtype=torch.bfloat16, device="cuda")
     lt = torch.from_numpy(lengths).cuda()
-    binding.op_attention(qkv, lt, H, nh, ctx)
+    binding.op_attention(attn_layout(qkv, H, nh), lt, H, nh, ctx)
     torch.cuda.synchronize()
     got = to_np(ctx)
     starts = inputs.offsets(lengths)
@@ -93,7 +103,7 @@ def test_attention_single_token_is_v(cuda_lib):
     rng = np.random.default_rng(3)
     qkv, qkv64 = bf16_tensor(rng.normal(0, 1.0, (5, 3 * H)))
     ctx = torch.empty(5, H, dtype=torch.bfloat16, device="cuda")
-    binding.op_attention(qkv, torch.from_numpy(lengths).cuda(), H, nh, ctx)
+    binding.op_attention(attn_layout(qkv, H, nh), torch.from_numpy(lengths).cuda(), H, nh, ctx)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(to_np(ctx), qkv64[:, 2 * H:])
 
