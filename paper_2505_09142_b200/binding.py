@@ -15,7 +15,8 @@ import numpy as np
 from . import inputs
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libelis.so")
+# ELIS_LIB selects an alternative in-tree build (A/B kernel experiments); default libelis.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 
 ELIS_OK = 0
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",

@@ -39,7 +39,11 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Compile + link libelis.so; a named `variant` (extra -D `defines`, e.g. the attention
+    phase tracer ELIS_ATTN_TRACE) builds libelis_<variant>.so from its own object directory."""
+    BUILD = os.path.join(ROOT, "build", "elis" + (f"_{variant}" if variant else ""))
+    LIB = os.path.join(PKG, f"libelis_{variant}.so" if variant else "libelis.so")
     os.makedirs(BUILD, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [
@@ -50,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([nvcc(), *NVCC_FLAGS, *inc, "-c", s, "-o", o])
+            jobs.append([nvcc(), *NVCC_FLAGS, *defines, *inc, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -76,4 +80,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var[0] if var else "", defines=defs))

@@ -11,10 +11,45 @@
 // products on mma.sync m16n8k16 bf16 -> fp32 (P rounded to bf16 for the PV product).
 // The whole K/V of one (request, head) is <= 512 x 64 x 2 x 2 B = 128 KB.
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace elis {
+
+#ifdef ELIS_ATTN_TRACE
+// Diagnostic build only (python -m paper_2505_09142_b200.build --variant=trace -DELIS_ATTN_TRACE):
+// thread 0 of every tcgen05 attention CTA stamps %globaltimer at its phase boundaries.
+constexpr size_t kTraceCap = 1 << 16;
+__device__ unsigned long long g_attn_trace[kTraceCap * 8];
+static void* g_attn_trace_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_attn_trace);
+  return p;
+}
+#define ATTN_TRACE(slot, val)                                                          \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      const size_t id_ = blockIdx.x;      \
+      if (id_ < kTraceCap) g_attn_trace[id_ * 8 + (slot)] = (val);                     \
+    }                                                                                  \
+  } while (0)
+__device__ __forceinline__ unsigned long long attn_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned attn_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#else
+#define ATTN_TRACE(slot, val) \
+  do {                        \
+  } while (0)
+#endif
 
 namespace {
 
@@ -53,19 +88,18 @@ ELIS_DEV void load_tile(uint16_t* s, const uint16_t* g, int ld, int row0, int L)
 
 template <int D>
 __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu,
-                                                   const int2* __restrict__ work, const int32_t* __restrict__ num_work,
-                                                   int H, uint16_t* __restrict__ ctx, float scale_log2) {
+                                                   const AttnWork* __restrict__ work,
+                                                   const int32_t* __restrict__ num_work, int H, int nh,
+                                                   uint16_t* __restrict__ ctx, float scale_log2) {
   constexpr int LDS = D + 8;  // padded row: conflict-free ldmatrix
   __shared__ __align__(16) uint16_t sQ[BQ * LDS];
   __shared__ __align__(16) uint16_t sK[2][BKV * LDS];
   __shared__ __align__(16) uint16_t sV[2][BKV * LDS];
 
-  if (static_cast<int>(blockIdx.x) >= __ldg(num_work)) return;
-  const int2 w = work[blockIdx.x];
-  const int req = w.x, q0 = w.y;
-  const int start = __ldg(cu + req);
-  const int L = __ldg(cu + req + 1) - start;
-  const int h = blockIdx.y;
+  const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
+  if (item >= __ldg(num_work)) return;
+  const AttnWork w = work[item];
+  const int start = w.start, L = w.len, q0 = w.q0;
   const int ld = 3 * H;
   const uint16_t* gQ = qkv + static_cast<size_t>(start) * ld + h * D;
   const uint16_t* gK = gQ + H;
@@ -216,11 +250,49 @@ constexpr int TD = 64;         // head dim
 constexpr int kBlkBytes = TKB * TD * 2;  // 16 KB
 constexpr int kAttnTcSmem = 3 * kBlkBytes + 1024 + 256;
 constexpr uint32_t kOCol = 64;
+// packed fp32 pairs (Blackwell FFMA2 / FADD2: two lanes of fp32 math per instruction)
+ELIS_DEV unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+ELIS_DEV void f2_unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+ELIS_DEV unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+ELIS_DEV unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+ELIS_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+ELIS_DEV float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __global__ void __launch_bounds__(128, 4)
-    k_attention_tc(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ cu,
-                   const int2* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
+    k_attention_tc(const __grid_constant__ CUtensorMap tm,
+                   const AttnWork* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
                    uint16_t* __restrict__ ctx, float scale_log2, int Tp) {
-  if (static_cast<int>(blockIdx.x) >= __ldg(num_work)) return;
+#ifdef ELIS_ATTN_TRACE
+  const unsigned long long t_start = attn_gtime();
+#endif
+  // the work entry is read together with num_work (the list has capacity for every CTA; entries
+  // past num_work are never used) and carries the request bounds: no dependent loads
+  const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
+  const AttnWork w = work[item];
+  if (item >= __ldg(num_work)) return;
+  ATTN_TRACE(0, t_start);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -235,16 +307,12 @@ __global__ void __launch_bounds__(128, 4)
   uint64_t* o_full = bars + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
 
-  const int2 w = work[blockIdx.x];
-  const int req = w.x, q0 = w.y;
-  const int start = __ldg(cu + req);
-  const int L = __ldg(cu + req + 1) - start;
-  const int h = blockIdx.y;
+  const int start = w.start, L = w.len, q0 = w.q0;
   const int nkb = (L + TKB - 1) / TKB;  // 1..4
   const int warp = warp_id(), lane = lane_id();
   const bool issuer = threadIdx.x == 0;
 
-  if (issuer) {
+  if (issuer) {  // barriers + the first loads go out before the TMEM allocation / CTA barrier
     tma_prefetch_desc(&tm);
     mbar_init(q_full, 1);
     mbar_init(k_full, 1);
@@ -252,30 +320,31 @@ __global__ void __launch_bounds__(128, 4)
     mbar_init(s_full, 1);
     mbar_init(o_full, 1);
     fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<128>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  const int row = warp * 32 + lane;
-
-  constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
-  constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B (V) is MN-major
-  if (issuer) {
     mbar_arrive_expect_tx(q_full, kBlkBytes);
     tma_load_2d(sQ, &tm, q_full, 0, h * Tp + start + q0);
     mbar_arrive_expect_tx(k_full, kBlkBytes);
     tma_load_2d(sK, &tm, k_full, 0, (nh + h) * Tp + start);
     mbar_arrive_expect_tx(v_full, kBlkBytes);
     tma_load_2d(sV, &tm, v_full, 0, (2 * nh + h) * Tp + start);
-    mbar_wait(q_full, 0);
   }
+  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  ATTN_TRACE(1, attn_gtime());
+  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int row = warp * 32 + lane;
+  // warps whose 32 query rows all lie beyond L skip the softmax (their rows are never stored;
+  // MMA rows are independent)
+  const bool warp_active = q0 + warp * 32 < L;
+
+  constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
+  constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B (V) is MN-major
+  if (issuer) mbar_wait(q_full, 0);
   float m = -INFINITY, l = 0.f;   // running row max (scaled, log2 domain) and row sum
-  float o[TD];
-#pragma unroll
-  for (int i = 0; i < TD; ++i) o[i] = 0.f;
+  unsigned long long o2[TD / 2];  // O as fp32 pairs
+  const unsigned long long zero2 = f2_pack(0.f, 0.f);
 
   for (int j = 0; j < nkb; ++j) {
     const uint32_t ph = j & 1;
@@ -291,71 +360,81 @@ __global__ void __launch_bounds__(128, 4)
     }
     mbar_wait(s_full, ph);
     tc_fence_after();
+    if (j == 0) ATTN_TRACE(2, attn_gtime());
     if (issuer && j + 1 < nkb) {  // the S MMA has consumed K_j: prefetch K_{j+1}
       mbar_arrive_expect_tx(k_full, kBlkBytes);
       tma_load_2d(sK, &tm, k_full, 0, (nh + h) * Tp + start + (j + 1) * TKB);
     }
     const int nvalid_blk = L - j * TKB;  // keys >= L belong to other requests: masked
-    // 32-key chunks holding valid keys; warps whose 32 query rows all lie beyond L skip the
-    // softmax (their rows are never stored; MMA rows are independent)
-    const int nch = min(TKB / 32, (nvalid_blk + 31) / 32);
-    const bool warp_active = q0 + warp * 32 < L;
+    // 32-key chunks holding valid keys
+    const int nch = warp_active ? min(TKB / 32, (nvalid_blk + 31) / 32) : 0;
     // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM).
-    // Only the chunk holding the last valid key is masked; full chunks take a plain max tree.
+    // Only the chunk holding the last valid key is masked.
     uint32_t r[32];
     float bm = -INFINITY;
-#pragma unroll 1
-    for (int c = 0; c < (warp_active ? nch : 0); ++c) {
-      tmem_ld_32x32b_x32(taddr + c * 32, r);
-      tc_wait_ld();
-      const int nv = nvalid_blk - c * 32;
-      if (nv >= 32) {
-        float t[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) t[e] = fmaxf(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+    for (int c = 0; c < TKB / 32; ++c) {
+      if (c < nch) {
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tc_wait_ld();
+        const int nv = nvalid_blk - c * 32;
+        if (nv < 32) {
 #pragma unroll
-        for (int w = 8; w >= 1; w >>= 1)
+          for (int e = 0; e < 32; ++e)
+            if (e >= nv) r[e] = __float_as_uint(-INFINITY);
+        }
+        float t[11];
 #pragma unroll
-          for (int e = 0; e < w; ++e) t[e] = fmaxf(t[e], t[e + w]);
-        bm = fmaxf(bm, t[0]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (e < nv) bm = fmaxf(bm, __uint_as_float(r[e]));
+        for (int e = 0; e < 10; ++e)
+          t[e] = fmax3(__uint_as_float(r[3 * e]), __uint_as_float(r[3 * e + 1]), __uint_as_float(r[3 * e + 2]));
+        t[10] = fmax3(__uint_as_float(r[30]), __uint_as_float(r[31]), bm);
+        bm = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmax3(t[6], t[7], fmax3(t[8], t[9], t[10])));
       }
     }
     const float m_new = fmaxf(m, bm * scale_log2);  // finite: every block has >= 1 valid key
-    float alpha;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(alpha) : "f"(m - m_new));  // 0 on the first block
+    const float alpha = ex2_approx(m - m_new);      // 0 on the first block
     m = m_new;
     // pass B: p = exp2(s*scale - m), block sum, P (bf16 pairs) over consumed score columns
-    float bl = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < (warp_active ? nch : 0); ++c) {
-      tmem_ld_32x32b_x32(taddr + c * 32, r);
-      tc_wait_ld();
-      const int nv = nvalid_blk - c * 32;
-      float p[32];
+    const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
+    const unsigned long long nm2 = f2_pack(-m, -m);
+    unsigned long long acc0 = zero2, acc1 = zero2;  // 2 x 2 independent partial sums, fixed order
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p[e]) : "f"(fmaf(__uint_as_float(r[e]), scale_log2, -m)));
-      if (nv < 32) {
+    for (int c = 0; c < TKB / 32; ++c) {
+      if (c < nch) {
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tc_wait_ld();
+        const int nv = nvalid_blk - c * 32;
+        float p[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) p[e] = (e < nv) ? p[e] : 0.f;
+        for (int e = 0; e < 16; ++e) {
+          float x0, x1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+          p[2 * e] = ex2_approx(x0);
+          p[2 * e + 1] = ex2_approx(x1);
+        }
+        if (nv < 32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) p[e] = (e < nv) ? p[e] : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc0 = f2_add(acc0, f2_pack(p[4 * e], p[4 * e + 1]));
+          acc1 = f2_add(acc1, f2_pack(p[4 * e + 2], p[4 * e + 3]));
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
+        tmem_st_32x32b_x16(taddr + c * 16, pk);
       }
-      float sacc[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial sums, fixed order
-#pragma unroll
-      for (int e = 0; e < 32; ++e) sacc[e & 3] += p[e];
-      bl += (sacc[0] + sacc[1]) + (sacc[2] + sacc[3]);
-      uint32_t pk[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
-      tmem_st_32x32b_x16(taddr + c * 16, pk);
     }
-    l = l * alpha + bl;
+    float a0, a1, a2, a3;
+    f2_unpack(acc0, a0, a1);
+    f2_unpack(acc1, a2, a3);
+    l = l * alpha + ((a0 + a1) + (a2 + a3));
     tc_wait_st();
     tc_fence_before();
     __syncthreads();  // P_j complete in TMEM (all 128 rows)
+    if (j == 0) ATTN_TRACE(3, attn_gtime());
     if (issuer) {
       tc_fence_after();
       mbar_wait(v_full, ph);
@@ -368,24 +447,36 @@ __global__ void __launch_bounds__(128, 4)
     }
     mbar_wait(o_full, ph);
     tc_fence_after();
+    if (j == 0) ATTN_TRACE(4, attn_gtime());
     if (issuer && j + 1 < nkb) {  // the PV MMA has consumed V_j: prefetch V_{j+1}
       mbar_arrive_expect_tx(v_full, kBlkBytes);
       tma_load_2d(sV, &tm, v_full, 0, (2 * nh + h) * Tp + start + (j + 1) * TKB);
     }
+    // O = alpha O + O_j  (the first block just takes O_0)
+    if (warp_active) {
+      const unsigned long long al2 = f2_pack(alpha, alpha);
 #pragma unroll
-    for (int hf = 0; hf < (warp_active ? 2 : 0); ++hf) {
-      tmem_ld_32x32b_x32(taddr + kOCol + hf * 32, r);
-      tc_wait_ld();
+      for (int hf = 0; hf < 2; ++hf) {
+        tmem_ld_32x32b_x32(taddr + kOCol + hf * 32, r);
+        tc_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) o[hf * 32 + i] = fmaf(o[hf * 32 + i], alpha, __uint_as_float(r[i]));
+        for (int i = 0; i < 16; ++i) {
+          const unsigned long long oj = f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          o2[hf * 16 + i] = (j == 0) ? oj : f2_fma(o2[hf * 16 + i], al2, oj);
+        }
+      }
     }
     tc_fence_before();
     __syncthreads();  // every row has read O_j before the next S MMA overwrites columns [0, 128)
+    if (j == 0) ATTN_TRACE(5, attn_gtime());
   }
   // epilogue: ctx = O / l (bf16)
   if (q0 + row < L) {
     const float inv = 1.0f / l;
     uint4* dst = reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + row) * H + h * TD);
+    float o[TD];
+#pragma unroll
+    for (int i = 0; i < TD / 2; ++i) f2_unpack(o2[i], o[2 * i], o[2 * i + 1]);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       dst[k] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
@@ -399,8 +490,11 @@ __global__ void __launch_bounds__(128, 4)
     tc_fence_after();
     tmem_dealloc<128>(tmem);
   }
+#ifdef ELIS_ATTN_TRACE
+  ATTN_TRACE(6, attn_gtime());
+  ATTN_TRACE(7, (static_cast<unsigned long long>(attn_smid()) << 32) | (static_cast<unsigned>(L) << 8) | nkb);
+#endif
 }
-
 
 }  // namespace
 
@@ -412,25 +506,32 @@ bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
 }
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
-                             const int2* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
+                             const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
                              int64_t plane_rows, uint16_t* ctx, cudaStream_t st) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
   const int64_t max_tiles = attn_max_tiles(T, n, attn_tile_q(d));
-  dim3 grid(static_cast<unsigned>(max_tiles), static_cast<unsigned>(num_heads));
+  const unsigned grid = static_cast<unsigned>(max_tiles * num_heads);
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
     if (e != cudaSuccess) return e;
-    k_attention_tc<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, cu_seqlens, work, num_work, H, num_heads, ctx,
-                                                   scale_log2, static_cast<int>(plane_rows));
+    k_attention_tc<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
+                                                   static_cast<int>(plane_rows));
   } else if (d == 32) {
-    k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, ctx, scale_log2);
+    k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, num_heads, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
+
+#ifdef ELIS_ATTN_TRACE
+extern "C" int elis_debug_attn_trace(unsigned long long* host, size_t n, int reset) {
+  if (reset) return static_cast<int>(cudaMemset(g_attn_trace_ptr(), 0, sizeof(g_attn_trace)));
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_attn_trace, std::min(n, kTraceCap * 8) * 8));
+}
+#endif
 
 }  // namespace elis

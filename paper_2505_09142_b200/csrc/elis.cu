@@ -140,7 +140,7 @@ struct elis_predictor {
   float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
   uint16_t *hb = nullptr, *qkv = nullptr, *ctx = nullptr, *g = nullptr;
   int32_t* cu = nullptr;
-  int2* work = nullptr;
+  AttnWork* work = nullptr;
   int32_t* num_work = nullptr;
   uint32_t* err = nullptr;
   int64_t max_tiles = 0;
@@ -378,7 +378,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   p->tile_q = attn_tile_q(H / cfg->num_heads);
   p->max_tiles = attn_work_capacity(T, N, p->tile_q);
   ALLOC(p->work, p->max_tiles);
-  ALLOC(p->num_work, 3);
+  ALLOC(p->num_work, 1);
   ALLOC(p->err, 1);
   ALLOC(p->pooled, static_cast<size_t>(N) * H);
   ALLOC(p->z0, static_cast<size_t>(N) * cfg->head_hidden);
@@ -724,12 +724,12 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   if (d == 64 && !make_tmap_qkv(&tm, qkv, static_cast<uint64_t>(T), hidden))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
   int32_t *cu = nullptr, *nw = nullptr;
-  int2* work = nullptr;
+  AttnWork* work = nullptr;
   uint32_t* err = nullptr;
   CUDA_TRY(cudaMalloc(&cu, (n + 1) * 4));
-  CUDA_TRY(cudaMalloc(&nw, 3 * 4));
+  CUDA_TRY(cudaMalloc(&nw, 4));
   CUDA_TRY(cudaMalloc(&err, 4));
-  CUDA_TRY(cudaMalloc(&work, tiles * sizeof(int2)));
+  CUDA_TRY(cudaMalloc(&work, tiles * sizeof(AttnWork)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
   CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, st));

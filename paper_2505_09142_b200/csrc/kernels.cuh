@@ -49,10 +49,18 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
 cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st);
 
 // ---- varlen metadata / embedding / LayerNorm (norm.cu)
-// lengths[n] -> cu_seqlens[n+1], attention work list (request, q0) with q tiles of tile_q
-// rows, and its size; validates lengths and their sum.
+// One attention work item: q rows [q0, q0 + tile_q) of the request at token offset `start`
+// with `len` tokens (the request bounds travel with the item: no dependent cu_seqlens load).
+struct __align__(16) AttnWork {
+  int32_t start, len, q0, req;
+};
+// Work-list cost classes: keys a tile attends to, in 128-key blocks (1..4 for L <= 512).
+constexpr int kAttnCostClasses = 4;
+// lengths[n] -> cu_seqlens[n+1], attention work list with q tiles of tile_q rows in
+// descending cost class (longest-processing-time-first: the long tiles start in the first
+// wave, the short ones fill the tail), and its size; validates lengths and their sum.
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        int2* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st);
+                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st);
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
                             int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
                             const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
@@ -63,18 +71,16 @@ cudaError_t launch_layernorm(const float* u, const float* gamma, const float* be
 // ---- attention (attention.cu)
 // head dim 64: tcgen05 kernel with 128-row q tiles; head dim 32: mma.sync, 64-row tiles.
 inline int attn_tile_q(int head_dim) { return head_dim == 64 ? 128 : 64; }
-inline int attn_num_buckets(int) { return 1; }
-inline int64_t attn_bucket_capacity(int64_t, int) { return 0; }
 // upper bound on the number of q-tiles for T tokens in n requests
 inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q - 1) / tile_q + n; }
 // total work-list entries to allocate for (T, n)
 inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_max_tiles(T, n, tile_q); }
 // head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
-// work / num_work: attn_num_buckets(tile_q) lists of attn_bucket_capacity(T, n) entries
+// grid: one CTA per (work item, head), head fastest, so the list's cost order is the launch order
 // head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H]
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
-                             const int2* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
+                             const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
                              int64_t plane_rows, uint16_t* ctx, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)

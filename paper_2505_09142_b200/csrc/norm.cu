@@ -47,49 +47,54 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total_out) {
 
 __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict__ lengths, int n, long long total,
                                                        int max_position, int32_t* __restrict__ cu,
-                                                       int2* __restrict__ work, int32_t* __restrict__ num_work,
-                                                       uint32_t* __restrict__ err, int tile_q, int nbuckets,
-                                                       long long bucket_stride) {
+                                                       AttnWork* __restrict__ work, int32_t* __restrict__ num_work,
+                                                       uint32_t* __restrict__ err, int tile_q) {
   __shared__ int warp_tot[32];
-  __shared__ int s_total_len, s_total_tiles[3];
+  __shared__ int s_total_len, s_total_tiles[kAttnCostClasses];
   __shared__ uint32_t s_err;
   if (threadIdx.x == 0) s_err = 0;
   __syncthreads();
-  // bucket of a request by length (tcgen05 attention: <= 128 / <= 256 / <= 512 keys)
-  auto bucket = [&](int L) { return nbuckets == 1 ? 0 : (L <= 128 ? 0 : (L <= 256 ? 1 : 2)); };
+  // cost class: 128-key blocks a q tile of this request attends to
+  auto cls = [](int L) { return min(kAttnCostClasses - 1, (L - 1) / 128); };
   const int per = (n + kMetaThreads - 1) / kMetaThreads;
   const int i0 = min(n, static_cast<int>(threadIdx.x) * per), i1 = min(n, i0 + per);
-  int my_len = 0, my_tiles[3] = {0, 0, 0};
+  int my_len = 0, my_tiles[kAttnCostClasses] = {};
   uint32_t e = 0;
   for (int i = i0; i < i1; ++i) {
     int L = lengths[i];
     if (L < 1 || L > max_position) { e |= ERR_LENGTH; L = max(1, min(L, max_position)); }
     my_len += L;
-    my_tiles[bucket(L)] += (L + tile_q - 1) / tile_q;
+    my_tiles[cls(L)] += (L + tile_q - 1) / tile_q;
   }
   if (e) atomicOr(&s_err, e);
   const int len_off = block_exclusive_scan(my_len, warp_tot, &s_total_len);
-  int tile_off[3] = {0, 0, 0};
-  for (int b = 0; b < nbuckets; ++b) tile_off[b] = block_exclusive_scan(my_tiles[b], warp_tot, &s_total_tiles[b]);
+  int tile_off[kAttnCostClasses];
+  for (int c = 0; c < kAttnCostClasses; ++c) tile_off[c] = block_exclusive_scan(my_tiles[c], warp_tot, &s_total_tiles[c]);
   if (threadIdx.x == 0 && static_cast<long long>(s_total_len) != total) atomicOr(&s_err, ERR_TOTAL);
   __syncthreads();
   const bool ok = (s_err == 0);
+  // class c's tiles follow every longer class's (descending cost)
+  int base = 0;
+  for (int c = kAttnCostClasses - 1; c >= 0; --c) {
+    tile_off[c] += base;
+    base += s_total_tiles[c];
+  }
   int lo = len_off;
   for (int i = i0; i < i1; ++i) {
     int L = max(1, min(lengths[i], max_position));
     cu[i] = lo;
     if (ok) {
-      const int b = bucket(L);
+      const int c = cls(L);
       const int nt = (L + tile_q - 1) / tile_q;
-      int2* dst = work + b * bucket_stride + tile_off[b];
-      for (int t = 0; t < nt; ++t) dst[t] = make_int2(i, t * tile_q);
-      tile_off[b] += nt;
+      AttnWork* dst = work + tile_off[c];
+      for (int t = 0; t < nt; ++t) dst[t] = AttnWork{lo, L, t * tile_q, i};
+      tile_off[c] += nt;
     }
     lo += L;
   }
   if (threadIdx.x == 0) {
     cu[n] = s_total_len;
-    for (int b = 0; b < nbuckets; ++b) num_work[b] = ok ? s_total_tiles[b] : 0;
+    num_work[0] = ok ? base : 0;
     if (s_err) atomicOr(err, s_err);
   }
 }
@@ -230,10 +235,8 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ u, 
 }  // namespace
 
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        int2* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st) {
-  const int nb = attn_num_buckets(tile_q);
-  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err, tile_q, nb,
-                                     nb > 1 ? attn_bucket_capacity(total, n) : 0);
+                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st) {
+  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err, tile_q);
   return cudaGetLastError();
 }
 
