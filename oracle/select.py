@@ -38,29 +38,57 @@ def remaining_key(pred: np.float32, generated: int, head_predicts_total: bool) -
     return float(rem)
 
 
+def starvation_adjust(rem: float, waited: int, is_running: bool, boost_after: int, boost_amount: float,
+                      preempt_margin: float) -> float:
+    """Starvation control ("policies that can adjust
+    the frequency of preemption and prevent starvation"; reading R17):
+      aging: subtract boost_amount x floor(windows_waited / boost_after) from the
+        key (the max(0, .) floor is applied by the caller);
+      preemption margin: a running job's key is lowered by preempt_margin tokens, so a waiting
+        job displaces it only when predicted shorter by more than the margin.
+    fp32 arithmetic, one rounding per step (the precision the keys are compared in)."""
+    r = np.float32(rem)
+    if boost_amount != 0.0 and waited > 0:
+        r = np.float32(r - np.float32(np.float32(boost_amount) * np.float32(waited // boost_after)))
+    if is_running and preempt_margin != 0.0:
+        r = np.float32(r - np.float32(preempt_margin))
+    return float(r)
+
+
 def isrtf_select(pred, generated, batch_cap: int, policy: int = POLICY_ISRTF,
                  allow_preempt: bool = True, order=None, running=None,
-                 head_predicts_total: bool = False):
+                 head_predicts_total: bool = False, windows_waited=None, boost_after: int = 1,
+                 boost_amount: float = 0.0, preempt_margin: float = 0.0):
     """Return (out_ids int32 [batch_cap] padded with -1, out_count, preempted uint8 [n], nan_count).
 
     Sorted by (class, key, order) over eligible slots (generated >= 0), where
     class = 0 for every slot when allow_preempt, else 0 for running slots and 1
     for the rest (running jobs keep their slots); key = remaining tokens (ISRTF)
-    or 0 (FCFS: arrival rank alone decides)."""
+    or 0 (FCFS: arrival rank alone decides).  Optional starvation control
+    (ISRTF only): see starvation_adjust."""
     pred = np.asarray(pred, dtype=np.float32)
     generated = np.asarray(generated, dtype=np.int64)
     n = pred.shape[0]
     order = np.arange(n, dtype=np.uint64) if order is None else np.asarray(order, dtype=np.uint64)
     running = np.zeros(n, dtype=np.uint8) if running is None else np.asarray(running, dtype=np.uint8)
+    waited = None if windows_waited is None else np.asarray(windows_waited, dtype=np.int64)
+    if boost_after < 1:
+        raise ValueError("boost_after must be >= 1")
     nan_count = 0
     items = []
     for i in range(n):
         if generated[i] < 0:
             continue
         if policy == POLICY_ISRTF:
-            k = remaining_key(pred[i], int(generated[i]), head_predicts_total)
-            if math.isinf(k) and math.isnan(float(pred[i])):
+            p = np.float32(pred[i])
+            rem = np.float32(p - np.float32(generated[i])) if head_predicts_total else p
+            if math.isnan(float(rem)):
                 nan_count += 1
+                k = math.inf
+            else:
+                adj = starvation_adjust(float(rem), int(waited[i]) if waited is not None else 0,
+                                        bool(running[i]), boost_after, boost_amount, preempt_margin)
+                k = adj if adj > 0.0 else 0.0
         elif policy == POLICY_FCFS:
             k = 0.0
         else:
