@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define ELIS_ABI_VERSION 1
+#define ELIS_ABI_VERSION 2
 
 typedef enum {
   ELIS_OK = 0,
@@ -117,6 +117,21 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
                                    int32_t n, int64_t total_tokens, float* out_pred,
                                    const int32_t* out_slot, void* stream);
 
+/* Starvation control ("policies that can adjust the frequency of preemption and
+ * prevent starvation"; SPEC S:233, S:264 aging; reading R17).  ISRTF keys only, fp32,
+ * applied to remaining = max(0, .) inputs before the floor at 0:
+ *   remaining -= boost_amount * floor(windows_waited[i] / boost_after)   if windows_waited[i] > 0
+ *   remaining -= preempt_margin                                           if running[i]
+ * so a job waiting in its buffer gains priority with every batch it is passed over for, and a
+ * waiting job displaces a running one only when predicted shorter by more than the margin. */
+typedef struct {
+  const int32_t* windows_waited; /* DEVICE [n] batches the slot's node formed without it since it  */
+                                 /* last ran or arrived; NULL => no aging                          */
+  int32_t boost_after;           /* >= 1                                                           */
+  float boost_amount;            /* tokens per boost_after windows waited, >= 0                     */
+  float preempt_margin;          /* tokens, >= 0                                                    */
+} elis_starvation;
+
 /* Preemption controls and tie-break inputs (P:345-348 [Backend Worker]). */
 typedef struct {
   int32_t policy;            /* ELIS_POLICY_ISRTF or ELIS_POLICY_FCFS                               */
@@ -126,6 +141,7 @@ typedef struct {
   uint8_t* out_preempted;    /* DEVICE [n] running && !selected; NULL => not written                 */
   int32_t* out_count;        /* DEVICE [1] number of ids written; NULL => not written                */
   int32_t* out_nan_count;    /* DEVICE [1] NaN predictions seen (keyed as +inf); NULL => not written */
+  const elis_starvation* starvation; /* HOST struct; NULL => no aging, no margin                    */
 } elis_preempt;
 
 /* Batcher.batch (Alg. 1 line 19): the batch_cap eligible slots with the
@@ -140,6 +156,28 @@ typedef struct {
 elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_t* generated,
                               int32_t n, int32_t batch_cap, const elis_preempt* preempt,
                               int32_t* out_ids, void* stream);
+
+/* ---- per-node Priority Buffers ---------------------------------
+ * Load Balancer.get_min_load (Alg. 1 line 3): each of n_new jobs, in arrival order,
+ * goes to the node with the fewest assigned jobs (ties -> lowest node id), which then counts it.
+ *   node_load  DEVICE int32 [num_nodes], updated in place (the caller decrements a node's count
+ *              when one of its jobs finishes); 1 <= num_nodes <= 64.
+ *   out_node   DEVICE int32 [n_new]. */
+elis_status elis_assign_nodes(elis_predictor* p, int32_t* node_load, int32_t num_nodes, int32_t n_new,
+                              int32_t* out_node, void* stream);
+/* Batcher.batch per node ("multiple priority queues, where each queue stores jobs
+ * assigned to a specific node"; a batch is formed when a node becomes available): for every
+ * ready node w, elis_isrtf_select restricted to the slots with node[i] == w, in one launch.
+ *   node        DEVICE int32 [n]; slots with a node outside [0, num_nodes) are never selected.
+ *   node_ready  DEVICE uint8 [num_nodes] or NULL (all ready); a node that is not ready gets
+ *               count 0 and its running slots are not flagged (they are mid-window).
+ *   out_ids     DEVICE int32 [num_nodes * batch_cap]: node w's batch at w * batch_cap, -1 padded.
+ *   out_counts  DEVICE int32 [num_nodes].
+ *   preempt     as for elis_isrtf_select (out_count unused; out_preempted per slot, own node). */
+elis_status elis_isrtf_select_nodes(elis_predictor* p, const float* pred, const int32_t* generated,
+                                    const int32_t* node, const uint8_t* node_ready, int32_t n,
+                                    int32_t num_nodes, int32_t batch_cap, const elis_preempt* preempt,
+                                    int32_t* out_ids, int32_t* out_counts, void* stream);
 
 /* ---- multi-GPU (BASELINE.json configs[4]) ------------------------------------------------
  * One process per GPU.  The caller creates a 128-byte ncclUniqueId on rank 0

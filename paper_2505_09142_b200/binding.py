@@ -19,6 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 
 ELIS_OK = 0
+ABI_VERSION = 2  # include/elis.h ELIS_ABI_VERSION
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
           6: "nccl", 7: "device input"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
@@ -35,9 +36,27 @@ class ElisConfig(ctypes.Structure):
                 ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32)]
 
 
+class ElisStarvation(ctypes.Structure):
+    _fields_ = [("windows_waited", _vp), ("boost_after", _i32), ("boost_amount", _f32), ("preempt_margin", _f32)]
+
+
 class ElisPreempt(ctypes.Structure):
     _fields_ = [("policy", _i32), ("allow_preempt", _i32), ("order", _vp), ("running", _vp),
-                ("out_preempted", _vp), ("out_count", _vp), ("out_nan_count", _vp)]
+                ("out_preempted", _vp), ("out_count", _vp), ("out_nan_count", _vp),
+                ("starvation", ctypes.POINTER(ElisStarvation))]
+
+
+def _preempt(policy, allow_preempt, order, running, out_preempted, out_count, out_nan_count,
+             windows_waited=None, boost_after=1, boost_amount=0.0, preempt_margin=0.0):
+    """elis_preempt (+ elis_starvation when aging or a margin is requested); the returned
+    struct keeps its starvation struct alive."""
+    pre = ElisPreempt(policy, int(allow_preempt), _ptr(order), _ptr(running), _ptr(out_preempted),
+                      _ptr(out_count), _ptr(out_nan_count), None)
+    if windows_waited is not None or boost_amount or preempt_margin:
+        sv = ElisStarvation(_ptr(windows_waited), int(boost_after), float(boost_amount), float(preempt_margin))
+        pre._sv = sv
+        pre.starvation = ctypes.pointer(sv)
+    return pre
 
 
 class ElisError(RuntimeError):
@@ -65,6 +84,8 @@ def lib():
         "elis_nccl_unique_id": (_i32, [_vp]),
         "elis_dist_attach": (_i32, [_vp, _i32, _i32, _vp]),
         "elis_isrtf_select_dist": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+        "elis_assign_nodes": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp]),
+        "elis_isrtf_select_nodes": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
         "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp,
                                        _vp, _vp, _vp]),
         "elis_sync_status": (_i32, [_vp]),
@@ -115,7 +136,7 @@ def _stream(stream):
 
 def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
                 head_predicts_total: bool = False) -> ElisConfig:
-    return ElisConfig(1, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
+    return ElisConfig(ABI_VERSION, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
                       cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
                       int(head_predicts_total), int(max_tokens), int(max_requests), int(device))
 
@@ -155,11 +176,29 @@ class Predictor:
                                            _ptr(out_slot), _stream(stream)), "elis_predict_remaining")
 
     def isrtf_select(self, pred, generated, batch_cap: int, out_ids, policy=POLICY_ISRTF, allow_preempt=True,
-                     order=None, running=None, out_preempted=None, out_count=None, out_nan_count=None, stream=None):
-        pre = ElisPreempt(policy, int(allow_preempt), _ptr(order), _ptr(running), _ptr(out_preempted),
-                          _ptr(out_count), _ptr(out_nan_count))
+                     order=None, running=None, out_preempted=None, out_count=None, out_nan_count=None, stream=None,
+                     windows_waited=None, boost_after=1, boost_amount=0.0, preempt_margin=0.0):
+        pre = _preempt(policy, allow_preempt, order, running, out_preempted, out_count, out_nan_count,
+                       windows_waited, boost_after, boost_amount, preempt_margin)
         check(lib().elis_isrtf_select(self.h, _ptr(pred), _ptr(generated), int(generated.shape[0]), int(batch_cap),
                                       ctypes.byref(pre), _ptr(out_ids), _stream(stream)), "elis_isrtf_select")
+
+    def assign_nodes(self, node_load, n_new: int, out_node, stream=None):
+        """Least-loaded node for each of n_new arriving jobs; node_load (device int32) updated."""
+        check(lib().elis_assign_nodes(self.h, _ptr(node_load), int(node_load.shape[0]), int(n_new), _ptr(out_node),
+                                      _stream(stream)), "elis_assign_nodes")
+
+    def isrtf_select_nodes(self, pred, generated, node, num_nodes: int, batch_cap: int, out_ids, out_counts,
+                           node_ready=None, policy=POLICY_ISRTF, allow_preempt=True, order=None, running=None,
+                           out_preempted=None, out_nan_count=None, stream=None, windows_waited=None,
+                           boost_after=1, boost_amount=0.0, preempt_margin=0.0):
+        """Per-node batches: out_ids [num_nodes * batch_cap], out_counts [num_nodes] (device)."""
+        pre = _preempt(policy, allow_preempt, order, running, out_preempted, None, out_nan_count,
+                       windows_waited, boost_after, boost_amount, preempt_margin)
+        check(lib().elis_isrtf_select_nodes(self.h, _ptr(pred), _ptr(generated), _ptr(node), _ptr(node_ready),
+                                            int(generated.shape[0]), int(num_nodes), int(batch_cap),
+                                            ctypes.byref(pre), _ptr(out_ids), _ptr(out_counts), _stream(stream)),
+              "elis_isrtf_select_nodes")
 
     def dist_attach(self, rank: int, world: int, unique_id: bytes):
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
@@ -168,8 +207,7 @@ class Predictor:
     def isrtf_select_dist(self, pred, generated, global_offset: int, batch_cap: int, out_ids, policy=POLICY_ISRTF,
                           allow_preempt=True, order=None, running=None, out_preempted=None, out_count=None,
                           out_nan_count=None, stream=None):
-        pre = ElisPreempt(policy, int(allow_preempt), _ptr(order), _ptr(running), _ptr(out_preempted),
-                          _ptr(out_count), _ptr(out_nan_count))
+        pre = _preempt(policy, allow_preempt, order, running, out_preempted, out_count, out_nan_count)
         check(lib().elis_isrtf_select_dist(self.h, _ptr(pred), _ptr(generated), int(generated.shape[0]),
                                            int(global_offset), int(batch_cap), ctypes.byref(pre), _ptr(out_ids),
                                            _stream(stream)), "elis_isrtf_select_dist")

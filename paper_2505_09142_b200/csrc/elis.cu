@@ -385,7 +385,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   ALLOC(p->z1, static_cast<size_t>(N) * cfg->head_hidden);
   p->key_cap = std::max(N, 65536);
   ALLOC(p->sc.keys, p->key_cap);
-  ALLOC(p->sc.info, 8);
+  ALLOC(p->sc.info, 8 * kMaxNodes);
   ALLOC(p->sc.sel_keys, kMaxBatchCap);
   ALLOC(p->sc.sel_ids, kMaxBatchCap);
   ALLOC(p->tmp_ids, kMaxBatchCap);
@@ -472,7 +472,24 @@ static elis_status validate_select(elis_predictor* p, const float* pred, const i
   if (!out_ids || (n > 0 && (!pred || !generated))) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
   if (pre && pre->policy != ELIS_POLICY_ISRTF && pre->policy != ELIS_POLICY_FCFS)
     return fail(ELIS_ERR_INVALID_ARG, "policy");
+  if (pre && pre->starvation) {
+    const elis_starvation* sv = pre->starvation;
+    if (sv->boost_after < 1) return fail(ELIS_ERR_INVALID_ARG, "starvation.boost_after < 1");
+    if (!(sv->boost_amount >= 0.f) || !(sv->preempt_margin >= 0.f))
+      return fail(ELIS_ERR_INVALID_ARG, "starvation amounts must be >= 0");
+  }
   return ELIS_OK;
+}
+
+static Starvation starvation_of(const elis_preempt* pre) {
+  Starvation s{nullptr, 1, 0.f, 0.f};
+  if (pre && pre->starvation) {
+    s.waited = pre->starvation->windows_waited;
+    s.boost_after = pre->starvation->boost_after;
+    s.boost_amount = s.waited ? pre->starvation->boost_amount : 0.f;
+    s.margin = pre->starvation->preempt_margin;
+  }
+  return s;
 }
 
 elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_t* generated, int32_t n,
@@ -488,12 +505,53 @@ elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_
   const uint8_t* running = pre ? pre->running : nullptr;
   LAUNCH(p, PC_KEYS, st,
          launch_make_keys(pred, generated, order, running, n, policy, allow, p->cfg.head_predicts_total, 0u,
-                          p->sc.keys, p->sc.info, st));
+                          starvation_of(pre), p->sc.keys, p->sc.info, st));
   LAUNCH(p, PC_SELECT, st,
          launch_select_topk(p->sc.keys, nullptr, n, batch_cap, out_ids, pre ? pre->out_count : nullptr,
                             pre ? pre->out_nan_count : nullptr, p->sc, st));
   if (pre && pre->out_preempted)
     LAUNCH(p, PC_PREEMPT, st, launch_preempt_flags(p->sc.keys, running, n, p->sc.info, pre->out_preempted, st));
+  return ELIS_OK;
+}
+
+elis_status elis_assign_nodes(elis_predictor* p, int32_t* node_load, int32_t num_nodes, int32_t n_new,
+                              int32_t* out_node, void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (num_nodes < 1 || num_nodes > kMaxNodes) return fail(ELIS_ERR_INVALID_ARG, "num_nodes outside [1, 64]");
+  if (n_new < 0) return fail(ELIS_ERR_INVALID_ARG, "n_new < 0");
+  if (!node_load || (n_new > 0 && !out_node)) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->last_stream = st;
+  LAUNCH(p, PC_SELECT, st, launch_assign_nodes(node_load, num_nodes, n_new, out_node, st));
+  return ELIS_OK;
+}
+
+elis_status elis_isrtf_select_nodes(elis_predictor* p, const float* pred, const int32_t* generated,
+                                    const int32_t* node, const uint8_t* node_ready, int32_t n, int32_t num_nodes,
+                                    int32_t batch_cap, const elis_preempt* pre, int32_t* out_ids,
+                                    int32_t* out_counts, void* stream) {
+  elis_status s = validate_select(p, pred, generated, n, batch_cap, pre, out_ids);
+  if (s != ELIS_OK) return s;
+  if (num_nodes < 1 || num_nodes > kMaxNodes) return fail(ELIS_ERR_INVALID_ARG, "num_nodes outside [1, 64]");
+  if (!out_counts || (n > 0 && !node)) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->last_stream = st;
+  const int policy = pre ? pre->policy : ELIS_POLICY_ISRTF;
+  const int allow = pre ? pre->allow_preempt : 1;
+  const uint32_t* order = pre ? pre->order : nullptr;
+  const uint8_t* running = pre ? pre->running : nullptr;
+  LAUNCH(p, PC_KEYS, st,
+         launch_make_keys(pred, generated, order, running, n, policy, allow, p->cfg.head_predicts_total, 0u,
+                          starvation_of(pre), p->sc.keys, p->sc.info, st));
+  LAUNCH(p, PC_SELECT, st,
+         launch_select_topk_nodes(p->sc.keys, nullptr, node, node_ready, num_nodes, n, batch_cap, out_ids, out_counts,
+                                  pre ? pre->out_nan_count : nullptr, p->sc, st));
+  if (pre && pre->out_preempted)
+    LAUNCH(p, PC_PREEMPT, st,
+           launch_preempt_flags_nodes(p->sc.keys, running, node, node_ready, num_nodes, n, p->sc.info,
+                                      pre->out_preempted, st));
   return ELIS_OK;
 }
 
@@ -551,7 +609,7 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
   // 1. local keys (order defaults to the GLOBAL slot index) and local top-cap candidates
   LAUNCH(p, PC_KEYS, st,
          launch_make_keys(pred, generated, order, running, n_local, policy, allow, p->cfg.head_predicts_total,
-                          static_cast<uint32_t>(global_offset), p->sc.keys, p->sc.info, st));
+                          static_cast<uint32_t>(global_offset), starvation_of(pre), p->sc.keys, p->sc.info, st));
   LAUNCH(p, PC_SELECT, st,
          launch_select_topk(p->sc.keys, nullptr, n_local, batch_cap, p->tmp_ids, nullptr,
                             pre ? pre->out_nan_count : nullptr, p->sc, st));

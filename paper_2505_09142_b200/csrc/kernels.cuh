@@ -93,21 +93,39 @@ cudaError_t launch_head_out(const float* Z, const float* w, const float* b, int 
 
 // ---- ISRTF select (select.cu)
 constexpr int kMaxBatchCap = 4096;
+constexpr int kMaxNodes = 64;  // worker nodes of the per-node Priority Buffers
+// starvation control inputs of the key pack (R17); waited == nullptr: no aging
+struct Starvation {
+  const int32_t* waited;
+  int boost_after;
+  float boost_amount;
+  float margin;
+};
 struct SelectScratch {
   unsigned long long* keys;   // [n]
-  uint32_t* info;             // [8]: prefix lo/hi, mask lo/hi, count, n_elig, nan_count
+  uint32_t* info;             // [8 * kMaxNodes]: per node thr lo/hi, -, -, count, n_elig; [6] nan_count
   unsigned long long* sel_keys;  // [cap] selected keys in order (UINT64_MAX padded)
   int32_t* sel_ids;              // [cap]
 };
 cudaError_t launch_make_keys(const float* pred, const int32_t* generated, const uint32_t* order,
                              const uint8_t* running, int n, int policy, int allow_preempt, int head_predicts_total,
-                             uint32_t order_offset, unsigned long long* keys, uint32_t* info, cudaStream_t st);
+                             uint32_t order_offset, Starvation sv, unsigned long long* keys, uint32_t* info,
+                             cudaStream_t st);
 // top-cap over keys[n]; ids (optional) map position -> id; writes out_ids / out_count / scratch
 cudaError_t launch_select_topk(const unsigned long long* keys, const int32_t* ids, int n, int cap,
                                int32_t* out_ids, int32_t* out_count, int32_t* out_nan, SelectScratch sc,
                                cudaStream_t st);
 cudaError_t launch_preempt_flags(const unsigned long long* keys, const uint8_t* running, int n, const uint32_t* info,
                                  uint8_t* out_preempted, cudaStream_t st);
+// per-node variants (node == nullptr: one node); out_ids [num_nodes * cap], out_count [num_nodes]
+cudaError_t launch_select_topk_nodes(const unsigned long long* keys, const int32_t* ids, const int32_t* node,
+                                     const uint8_t* node_ready, int num_nodes, int n, int cap, int32_t* out_ids,
+                                     int32_t* out_count, int32_t* out_nan, SelectScratch sc, cudaStream_t st);
+cudaError_t launch_preempt_flags_nodes(const unsigned long long* keys, const uint8_t* running, const int32_t* node,
+                                       const uint8_t* node_ready, int num_nodes, int n, const uint32_t* info,
+                                       uint8_t* out_preempted, cudaStream_t st);
+// least-loaded assignment of n_new arriving jobs; load [num_nodes] updated in place
+cudaError_t launch_assign_nodes(int32_t* load, int num_nodes, int n_new, int32_t* out_node, cudaStream_t st);
 cudaError_t launch_pack_candidates(const SelectScratch sc, int cap, int global_offset, void* send, cudaStream_t st);
 cudaError_t launch_unpack_candidates(const void* recv, int total, unsigned long long* keys, int32_t* ids,
                                      cudaStream_t st);

@@ -28,7 +28,7 @@ constexpr unsigned long long KEY_NONE = 0xFFFFFFFFFFFFFFFFull;
 
 __global__ void k_make_keys(const float* __restrict__ pred, const int32_t* __restrict__ generated,
                             const uint32_t* __restrict__ order, const uint8_t* __restrict__ running, int n, int policy,
-                            int allow_preempt, int head_predicts_total, uint32_t order_offset,
+                            int allow_preempt, int head_predicts_total, uint32_t order_offset, Starvation sv,
                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ info) {
   uint32_t nan_local = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -39,6 +39,15 @@ __global__ void k_make_keys(const float* __restrict__ pred, const int32_t* __res
       if (policy == 0) {
         float rem = pred[i];
         if (head_predicts_total) rem = __fsub_rn(rem, static_cast<float>(g));
+        if (rem == rem) {
+          // starvation control (R17): aging, then the preemption
+          // margin of running jobs; explicit fp32 roundings (no contraction), as the oracle
+          if (sv.waited && sv.boost_amount != 0.f) {
+            const int wt = sv.waited[i];
+            if (wt > 0) rem = __fsub_rn(rem, __fmul_rn(sv.boost_amount, static_cast<float>(wt / sv.boost_after)));
+          }
+          if (sv.margin != 0.f && running && running[i]) rem = __fsub_rn(rem, sv.margin);
+        }
         if (rem != rem) {
           bits = 0x7F800000u;
           ++nan_local;
@@ -60,8 +69,13 @@ __global__ void k_make_keys(const float* __restrict__ pred, const int32_t* __res
 
 constexpr int kSelThreads = 1024;
 
+// One CTA per node (per-node Priority Buffers): block w selects among the slots with
+// node[i] == w (node == NULL: one block over every slot); a node that is not ready selects
+// nothing.  Outputs of block w: out_ids[w * cap ...], out_count[w], info[8 w + {0, 1, 4, 5}].
 __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long long* __restrict__ keys,
-                                                             const int32_t* __restrict__ ids, int n, int cap,
+                                                             const int32_t* __restrict__ ids,
+                                                             const int32_t* __restrict__ node,
+                                                             const uint8_t* __restrict__ node_ready, int n, int cap,
                                                              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                                                              int32_t* __restrict__ out_nan, uint32_t* __restrict__ info,
                                                              unsigned long long* __restrict__ sel_keys,
@@ -74,10 +88,20 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
   __shared__ unsigned long long s_prefix, s_mask;
 
   const int tid = threadIdx.x;
+  const int w = blockIdx.x;
+  const bool ready = !node_ready || node_ready[w];
+  out_ids += static_cast<size_t>(w) * cap;
+  if (out_count) out_count += w;
+  if (sel_keys) sel_keys += static_cast<size_t>(w) * cap;
+  if (sel_ids) sel_ids += static_cast<size_t>(w) * cap;
+  uint32_t* info_w = info + 8 * w;
+  // slot i takes part in this block's selection
+  auto mine = [&](int i, unsigned long long k) { return k != KEY_NONE && (!node || node[i] == w); };
   if (tid == 0) { s_elig = 0; s_count = 0; s_prefix = 0; s_mask = 0; s_done = 0; }
   __syncthreads();
   int e = 0;
-  for (int i = tid; i < n; i += kSelThreads) e += (keys[i] != KEY_NONE);
+  if (ready)
+    for (int i = tid; i < n; i += kSelThreads) e += mine(i, keys[i]);
   e = __reduce_add_sync(0xffffffffu, e);
   if (lane_id() == 0) atomicAdd(&s_elig, e);
   __syncthreads();
@@ -93,7 +117,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
       const unsigned long long prefix = s_prefix, mask = s_mask;
       for (int i = tid; i < n; i += kSelThreads) {
         const unsigned long long k = keys[i];
-        if (k != KEY_NONE && (k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
+        if (mine(i, k) && (k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1);
       }
       __syncthreads();
       if (tid < 32) {
@@ -134,9 +158,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
   // winners: eligible keys whose masked prefix <= prefix (all eligible if target == s_elig)
   const bool take_all = (target == s_elig);
   const unsigned long long prefix = s_prefix, mask = s_mask;
-  for (int i = tid; i < n; i += kSelThreads) {
+  for (int i = tid; i < (target > 0 ? n : 0); i += kSelThreads) {
     const unsigned long long k = keys[i];
-    if (k == KEY_NONE) continue;
+    if (!mine(i, k)) continue;
     if (take_all || (k & mask) <= prefix) {
       const int slot = atomicAdd(&s_count, 1);
       if (slot < sort_len) {
@@ -177,22 +201,82 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
     if (out_count) *out_count = target;
     // threshold = the target-th key: a slot is selected iff eligible and key <= threshold
     const unsigned long long thr = target > 0 ? ck[target - 1] : 0ull;
-    info[0] = static_cast<uint32_t>(thr);
-    info[1] = static_cast<uint32_t>(thr >> 32);
-    info[4] = static_cast<uint32_t>(target);
-    info[5] = static_cast<uint32_t>(s_elig);
-    if (out_nan) *out_nan = static_cast<int32_t>(info[6]);
+    info_w[0] = static_cast<uint32_t>(thr);
+    info_w[1] = static_cast<uint32_t>(thr >> 32);
+    info_w[4] = static_cast<uint32_t>(target);
+    info_w[5] = static_cast<uint32_t>(s_elig);
+    if (out_nan && w == 0) *out_nan = static_cast<int32_t>(info[6]);
   }
 }
 
-__global__ void k_preempt(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ running, int n,
-                          const uint32_t* __restrict__ info, uint8_t* __restrict__ out) {
-  const unsigned long long thr = (static_cast<unsigned long long>(info[1]) << 32) | info[0];
-  const bool any = info[4] > 0;
+// out[i] = running[i] && !selected[i]; with nodes, against the slot's own node's threshold and
+// only on ready nodes (a busy node's running jobs are mid-window); node ids outside
+// [0, num_nodes) are never flagged.
+__global__ void k_preempt(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ running,
+                          const int32_t* __restrict__ node, const uint8_t* __restrict__ node_ready, int num_nodes,
+                          int n, const uint32_t* __restrict__ info, uint8_t* __restrict__ out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const bool selected = any && k != KEY_NONE && k <= thr;
-    out[i] = (running && running[i] && !selected) ? 1 : 0;
+    const int w = node ? node[i] : 0;
+    bool flag = false;
+    if (running && running[i] && w >= 0 && w < num_nodes && (!node_ready || node_ready[w])) {
+      const uint32_t* iw = info + 8 * w;
+      const unsigned long long thr = (static_cast<unsigned long long>(iw[1]) << 32) | iw[0];
+      const unsigned long long k = keys[i];
+      flag = !(iw[4] > 0 && k != KEY_NONE && k <= thr);
+    }
+    out[i] = flag ? 1 : 0;
+  }
+}
+
+// Greedy least-loaded assignment (Alg. 1 line 3) of n_new jobs in arrival order,
+// computed in parallel: job j takes the j-th smallest pair (load_w + k, w), k >= 0, in
+// lexicographic order -- exactly the node the sequential argmin (ties -> lowest id) picks.
+// count(v) = sum_w max(0, v - load_w) pairs lie below level v; job j's level v is the largest
+// with count(v) <= j and its node the (j - count(v))-th, in id order, with load_w <= v.
+__global__ void __launch_bounds__(1024) k_assign_nodes(int32_t* __restrict__ load, int W, int n_new,
+                                                       int32_t* __restrict__ out_node) {
+  __shared__ long long s_load[kMaxNodes];
+  __shared__ long long s_lo;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) s_load[w] = load[w];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long lo = s_load[0];
+    for (int w = 1; w < W; ++w) lo = s_load[w] < lo ? s_load[w] : lo;
+    s_lo = lo;
+  }
+  __syncthreads();
+  const long long lo = s_lo;
+  auto count_below = [&](long long v) {
+    long long c = 0;
+    for (int w = 0; w < W; ++w) c += v > s_load[w] ? v - s_load[w] : 0;
+    return c;
+  };
+  auto level = [&](long long j, long long* r) {  // level of job j and its rank within the level
+    long long a = lo, b = lo + j + 1;           // count(a) = 0 <= j < j + 1 <= count(b)
+    while (b - a > 1) {
+      const long long mid = (a + b) >> 1;
+      if (count_below(mid) <= j) a = mid; else b = mid;
+    }
+    *r = j - count_below(a);
+    return a;
+  };
+  for (int j = threadIdx.x; j < n_new; j += blockDim.x) {
+    long long r;
+    const long long v = level(j, &r);
+    int pick = -1;
+    for (int w = 0; w < W && pick < 0; ++w)
+      if (s_load[w] <= v && r-- == 0) pick = w;
+    out_node[j] = pick;
+  }
+  if (n_new > 0) {
+    long long r_last;
+    const long long v_last = level(n_new - 1, &r_last);
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+      long long rank = 0;  // nodes before w at level v_last
+      for (int u = 0; u < w; ++u) rank += s_load[u] <= v_last;
+      const long long add = (v_last > s_load[w] ? v_last - s_load[w] : 0) + (s_load[w] <= v_last && rank <= r_last);
+      load[w] = static_cast<int32_t>(s_load[w] + add);
+    }
   }
 }
 
@@ -230,18 +314,26 @@ int next_pow2(int x) {
 
 cudaError_t launch_make_keys(const float* pred, const int32_t* generated, const uint32_t* order,
                              const uint8_t* running, int n, int policy, int allow_preempt, int head_predicts_total,
-                             uint32_t order_offset, unsigned long long* keys, uint32_t* info, cudaStream_t st) {
+                             uint32_t order_offset, Starvation sv, unsigned long long* keys, uint32_t* info,
+                             cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(info, 0, 8 * sizeof(uint32_t), st);
   if (e != cudaSuccess || n <= 0) return e;
   int blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
   k_make_keys<<<blocks, 256, 0, st>>>(pred, generated, order, running, n, policy, allow_preempt, head_predicts_total,
-                                      order_offset, keys, info);
+                                      order_offset, sv, keys, info);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_topk(const unsigned long long* keys, const int32_t* ids, int n, int cap, int32_t* out_ids,
                                int32_t* out_count, int32_t* out_nan, SelectScratch sc, cudaStream_t st) {
+  return launch_select_topk_nodes(keys, ids, nullptr, nullptr, 1, n, cap, out_ids, out_count, out_nan, sc, st);
+}
+
+cudaError_t launch_select_topk_nodes(const unsigned long long* keys, const int32_t* ids, const int32_t* node,
+                                     const uint8_t* node_ready, int num_nodes, int n, int cap, int32_t* out_ids,
+                                     int32_t* out_count, int32_t* out_nan, SelectScratch sc, cudaStream_t st) {
+  if (num_nodes < 1 || num_nodes > kMaxNodes) return cudaErrorInvalidValue;
   const int sort_len = next_pow2(cap < 2 ? 2 : cap);
   const size_t smem = static_cast<size_t>(sort_len) * (sizeof(unsigned long long) + sizeof(int32_t));
   static bool attr = false;
@@ -251,17 +343,31 @@ cudaError_t launch_select_topk(const unsigned long long* keys, const int32_t* id
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_select_topk<<<1, kSelThreads, smem, st>>>(keys, ids, n, cap, out_ids, out_count, out_nan, sc.info, sc.sel_keys,
-                                              sc.sel_ids, sort_len);
+  k_select_topk<<<num_nodes, kSelThreads, smem, st>>>(keys, ids, node, node_ready, n, cap, out_ids, out_count,
+                                                      out_nan, sc.info, node ? nullptr : sc.sel_keys,
+                                                      node ? nullptr : sc.sel_ids, sort_len);
   return cudaGetLastError();
 }
 
 cudaError_t launch_preempt_flags(const unsigned long long* keys, const uint8_t* running, int n, const uint32_t* info,
                                  uint8_t* out_preempted, cudaStream_t st) {
+  return launch_preempt_flags_nodes(keys, running, nullptr, nullptr, 1, n, info, out_preempted, st);
+}
+
+cudaError_t launch_preempt_flags_nodes(const unsigned long long* keys, const uint8_t* running, const int32_t* node,
+                                       const uint8_t* node_ready, int num_nodes, int n, const uint32_t* info,
+                                       uint8_t* out_preempted, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
-  k_preempt<<<blocks, 256, 0, st>>>(keys, running, n, info, out_preempted);
+  k_preempt<<<blocks, 256, 0, st>>>(keys, running, node, node_ready, num_nodes, n, info, out_preempted);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assign_nodes(int32_t* load, int num_nodes, int n_new, int32_t* out_node, cudaStream_t st) {
+  if (num_nodes < 1 || num_nodes > kMaxNodes) return cudaErrorInvalidValue;
+  if (n_new <= 0) return cudaSuccess;
+  k_assign_nodes<<<1, 1024, 0, st>>>(load, num_nodes, n_new, out_node);
   return cudaGetLastError();
 }
 

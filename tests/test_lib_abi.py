@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert binding.lib().elis_abi_version() == 1
+    assert binding.lib().elis_abi_version() == 2
 
 
 @pytest.mark.parametrize("name", ["tiny", "base", "large"])
