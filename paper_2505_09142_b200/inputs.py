@@ -300,6 +300,21 @@ def response_tokens(job_id: int, total: int, seed: int = 0) -> np.ndarray:
     return rng.integers(1000, VOCAB, total).astype(np.int32)
 
 
+NOISY_MAE_SCHEDULE = (19.9, 16.0, 12.5, 9.5, 7.0, 5.0)  # SPEC S:209 (tokens; anchored at P:359's MAE 19.923)
+
+
+def noisy_remaining(job_id: int, total: int, generated: int, seed: int = 0,
+                    mae_schedule=NOISY_MAE_SCHEDULE, window: int = WINDOW_K) -> float:
+    """NoisyIterative priority source: max(0, total + e - generated) with
+    e ~ Laplace(scale = mae_schedule[min(step, last)]), step = generated // window, seeded per
+    (job id, step) so a replay is independent of scheduling order.  A stand-in for the trained
+    predictor's error (its weights are not available): the draw is an input, not method arithmetic."""
+    step = generated // window
+    scale = mae_schedule[min(step, len(mae_schedule) - 1)]
+    e = _rng(SUB_PRED, 200000 + seed, job_id, step).laplace(0.0, scale)
+    return max(0.0, float(total) + float(e) - float(generated))
+
+
 def random_sched_state(n: int, seed: int = 0, frac_running: float = 0.05, frac_empty: float = 0.05):
     """generated (int32, <0 = empty slot), order (unique uint32 rank of (arrival, id)),
     running (uint8) for select tests."""

@@ -1,13 +1,15 @@
 """Closed-loop ISRTF iteration driver + stream simulator (
 BASELINE.json configs[3]: Poisson arrivals, ISRTF with preemption vs FCFS, predictor on GPU).
 
-It runs PAPER.md Algorithm 1 (alg:scheduler_flow) for one backend worker with the
-GPU hot path in the loop.  At every window boundary:
+It runs PAPER.md Algorithm 1 (alg:scheduler_flow) for W backend workers (per-node
+Priority Buffers and the least-loaded balancer) with the GPU hot path in the
+loop.  At every scheduling instant:
   * the due set -- new arrivals and the jobs that just ran a window (lines 10-18; jobs waiting
     in the Priority Buffer keep their cached priority, R8) -- is re-predicted by
     elis_predict_remaining straight into a device-resident in-flight table (out_slot);
-  * elis_isrtf_select picks the next batch over the whole table (line 19) with the
-    running flags of the previous batch (preemption);
+  * elis_isrtf_select_nodes picks the next batch of every free node from its own queue
+    (line 19) with the running flags of the node's previous batch (preemption,
+    P:345-348) and optional aging / preemption margin (row f3);
   * the backend is modelled as windows of K = 50 tokens ending early when a member finishes
     (P:341-342), lasting TTFT (first execution) + TPOT x tokens (Sec. 2.1).
 The LLM itself is out of scope: each job's response tokens are synthetic and
@@ -15,7 +17,9 @@ its true length is known to the simulator only.
 
 Priority sources: "gpu" (the BGE + 8-FC predictor; random-init weights carry no length
 signal, so this measures the mechanics and the per-iteration GPU overhead), "oracle" (true
-remaining tokens: the SRTF bound, written into the table) and policy FCFS.
+remaining tokens: the SRTF bound, written into the table), "noisy" (SPEC's NoisyIterative:
+true length + Laplace error with the MAE schedule, a stand-in for the trained predictor) and
+policy FCFS.
 
 Every GPU decision is recorded so tests can replay the run through the fp64 oracle simulator
 and require identical schedules.
@@ -66,104 +70,161 @@ def build_sequence(prompt: np.ndarray, response: np.ndarray, generated: int, max
 
 
 class StreamSim:
+    """Algorithm 1 over `workers` backend nodes with per-node Priority Buffers:
+    arrivals go to the least-loaded node (elis_assign_nodes), every free node forms its batch
+    from its own queue in one elis_isrtf_select_nodes launch, with optional starvation control
+    (aging / preemption margin, R17).  Event order at an instant t (R18): windows
+    ending at t complete, arrivals up to t are admitted, free nodes form batches."""
+
     def __init__(self, predictor: binding.Predictor | None, policy: int = POLICY_ISRTF, cap: int = 4,
                  window: int = inputs.WINDOW_K, ttft_ms: float = 0.0, tpot_ms: float = 1.0,
-                 allow_preempt: bool = True, priority: str = "gpu", seed: int = 0):
+                 allow_preempt: bool = True, priority: str = "gpu", seed: int = 0, workers: int = 1,
+                 boost_after: int = 1, boost_amount: float = 0.0, preempt_margin: float = 0.0):
         if priority == "gpu" and predictor is None and policy == POLICY_ISRTF:
             raise ValueError("priority='gpu' needs a predictor")
         self.P = predictor
         self.policy, self.cap, self.K = policy, cap, window
         self.ttft, self.tpot, self.allow = ttft_ms, tpot_ms, allow_preempt
-        self.priority, self.seed = priority, seed
+        self.priority, self.seed, self.W = priority, seed, workers
+        self.boost_after, self.boost_amount, self.margin = boost_after, boost_amount, preempt_margin
 
     def run(self, prompts, totals, arrivals_ms, select_predictor: binding.Predictor | None = None) -> StreamResult:
         import torch
         P = self.P if self.P is not None else select_predictor
         if P is None:
             raise ValueError("a predictor (for the device select) is required")
-        nj = len(prompts)
+        nj, W, cap = len(prompts), self.W, self.cap
         order = np.argsort(arrivals_ms, kind="stable")
         assert (order == np.arange(nj)).all(), "jobs must be sorted by arrival (id = arrival rank)"
         responses = [inputs.response_tokens(j, int(totals[j]), self.seed) for j in range(nj)]
         gen = np.full(nj, -1, np.int32)            # -1: not arrived or finished (ineligible slot)
+        node_of = np.full(nj, -1, np.int32)
+        waited = np.zeros(nj, np.int32)
         first = np.full(nj, np.nan)
         finish = np.full(nj, np.nan)
         running = np.zeros(nj, np.uint8)
         started = np.zeros(nj, bool)
+        free_at = [None] * W
+        batch_of: list[list[int]] = [[] for _ in range(W)]
+        tokens_of = [0] * W
         dev = torch.device("cuda")
         st = torch.cuda.current_stream()
         d_table = torch.zeros(nj, device=dev)
         d_gen = torch.empty(nj, dtype=torch.int32, device=dev)
         d_run = torch.empty(nj, dtype=torch.uint8, device=dev)
+        d_node = torch.empty(nj, dtype=torch.int32, device=dev)
+        d_wait = torch.empty(nj, dtype=torch.int32, device=dev)
+        d_ready = torch.empty(W, dtype=torch.uint8, device=dev)
+        d_load = torch.zeros(W, dtype=torch.int32, device=dev)
+        d_newnode = torch.empty(max(nj, 1), dtype=torch.int32, device=dev)
         d_order = torch.arange(nj, dtype=torch.int32, device=dev).to(torch.int32)
-        d_ids = torch.empty(self.cap, dtype=torch.int32, device=dev)
-        d_cnt = torch.empty(1, dtype=torch.int32, device=dev)
-        h_ids = torch.empty(self.cap, dtype=torch.int32).pin_memory()
-        h_cnt = torch.empty(1, dtype=torch.int32).pin_memory()
+        d_ids = torch.empty(W * cap, dtype=torch.int32, device=dev)
+        d_cnt = torch.empty(W, dtype=torch.int32, device=dev)
+        h_ids = torch.empty(W * cap, dtype=torch.int32).pin_memory()
+        h_cnt = torch.empty(W, dtype=torch.int32).pin_memory()
+        aging = self.boost_amount != 0.0
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         recorded = {}
-        t = 0.0
         nxt = 0                                     # next job to arrive
         due: list[int] = []
-        iters, gpu_ms, host_ms, due_total = 0, 0.0, 0.0, 0
+        iters, selects, gpu_ms, host_ms, due_total = 0, 0, 0.0, 0.0, 0
         done = 0
         while done < nj:
-            while nxt < nj and arrivals_ms[nxt] <= t:
-                gen[nxt] = 0
-                due.append(nxt)
-                nxt += 1
-            if not (gen >= 0).any():
-                t = float(arrivals_ms[nxt])
-                running[:] = 0
-                continue
+            ends = [f for f in free_at if f is not None]
+            t = min(min(ends) if ends else np.inf, float(arrivals_ms[nxt]) if nxt < nj else np.inf)
             h0 = time.perf_counter()
+            # (a) windows ending at t
+            for w in range(W):
+                if free_at[w] is not None and free_at[w] <= t:
+                    running[node_of == w] = 0
+                    for j in batch_of[w]:
+                        gen[j] += tokens_of[w]
+                        if gen[j] >= totals[j]:
+                            finish[j] = free_at[w]
+                            gen[j] = -1
+                            done += 1
+                            d_load[w] -= 1
+                        else:
+                            running[j] = 1
+                            due.append(j)
+                    free_at[w], batch_of[w] = None, []
+            # (b) arrivals: least-loaded node on the device
+            n_new = 0
+            while nxt + n_new < nj and arrivals_ms[nxt + n_new] <= t:
+                n_new += 1
             ev0.record(st)
+            if n_new:
+                P.assign_nodes(d_load, n_new, d_newnode, stream=st)
+                node_of[nxt:nxt + n_new] = d_newnode[:n_new].cpu().numpy()
+                gen[nxt:nxt + n_new] = 0
+                waited[nxt:nxt + n_new] = 0
+                due.extend(range(nxt, nxt + n_new))
+                nxt += n_new
+            # (c) free nodes with work form their batches (one segmented select)
+            ready = np.array([free_at[w] is None for w in range(W)], np.uint8)
+            has_work = np.zeros(W, bool)
+            live = gen >= 0
+            has_work[np.unique(node_of[live])] = True
+            for w in range(W):
+                if ready[w] and not has_work[w]:
+                    running[node_of == w] = 0
+            if not (ready.astype(bool) & has_work).any():
+                ev1.record(st)
+                continue
             if due and self.policy == POLICY_ISRTF:
                 if self.priority == "gpu":
                     seqs = [build_sequence(prompts[j], responses[j], int(gen[j])) for j in due]
-                    lens = np.array([s.size for s in seqs], np.int32)
+                    lens = np.array([q.size for q in seqs], np.int32)
                     toks = torch.from_numpy(np.concatenate(seqs)).to(dev, non_blocking=True)
                     slots = torch.from_numpy(np.array(due, np.int32)).to(dev, non_blocking=True)
                     P.predict_remaining(toks, torch.from_numpy(lens).to(dev, non_blocking=True), int(lens.sum()),
                                         d_table, out_slot=slots, stream=st)
-                else:  # "oracle": true remaining tokens (SRTF bound)
-                    rem = (totals[due] - gen[due]).astype(np.float32)
+                else:  # "oracle": true remaining tokens (SRTF bound); "noisy": SPEC NoisyIterative
+                    if self.priority == "noisy":
+                        rem = np.array([inputs.noisy_remaining(j, int(totals[j]), int(gen[j]), self.seed)
+                                        for j in due], np.float32)
+                    else:
+                        rem = (totals[due] - gen[due]).astype(np.float32)
                     d_table[torch.from_numpy(np.array(due, np.int64)).to(dev)] = torch.from_numpy(rem).to(dev)
             d_gen.copy_(torch.from_numpy(gen), non_blocking=True)
             d_run.copy_(torch.from_numpy(running), non_blocking=True)
-            P.isrtf_select(d_table, d_gen, self.cap, d_ids, policy=self.policy, allow_preempt=self.allow,
-                           order=d_order, running=d_run, out_count=d_cnt, stream=st)
+            d_node.copy_(torch.from_numpy(node_of), non_blocking=True)
+            d_ready.copy_(torch.from_numpy(ready), non_blocking=True)
+            if aging:
+                d_wait.copy_(torch.from_numpy(waited), non_blocking=True)
+            P.isrtf_select_nodes(d_table, d_gen, d_node, W, cap, d_ids, d_cnt, node_ready=d_ready,
+                                 policy=self.policy, allow_preempt=self.allow, order=d_order, running=d_run,
+                                 stream=st, windows_waited=d_wait if aging else None, boost_after=self.boost_after,
+                                 boost_amount=self.boost_amount, preempt_margin=self.margin)
             h_ids.copy_(d_ids, non_blocking=True)
             h_cnt.copy_(d_cnt, non_blocking=True)
             ev1.record(st)
             st.synchronize()
             gpu_ms += ev0.elapsed_time(ev1)
+            selects += 1
             if due and self.policy == POLICY_ISRTF:
                 vals = d_table[torch.from_numpy(np.array(due, np.int64)).to(dev)].cpu().numpy()
                 for j, v in zip(due, vals):
                     recorded[(int(j), int(gen[j]))] = float(v)
             due_total += len(due)
-            batch = [int(x) for x in h_ids.numpy()[:int(h_cnt.item())]]
-            assert batch, "select returned an empty batch with eligible jobs"
-            w = min(self.K, min(int(totals[j] - gen[j]) for j in batch))
-            dur = (self.ttft if any(not started[j] for j in batch) else 0.0) + self.tpot * w
-            for j in batch:
-                if not started[j]:
-                    started[j] = True
-                    first[j] = t
-            t += dur
-            running[:] = 0
             due = []
-            for j in batch:
-                gen[j] += w
-                if gen[j] >= totals[j]:
-                    finish[j] = t
-                    gen[j] = -1
-                    done += 1
-                else:
-                    running[j] = 1
-                    due.append(j)
-            iters += 1
+            ids_all, cnts = h_ids.numpy().reshape(W, cap), h_cnt.numpy()
+            for w in range(W):
+                if not ready[w] or not has_work[w]:
+                    continue
+                batch = [int(x) for x in ids_all[w, :int(cnts[w])]]
+                assert batch, "select returned an empty batch for a node with eligible jobs"
+                mine = live & (node_of == w)
+                waited[mine] += 1
+                waited[batch] = 0
+                tok = min(self.K, min(int(totals[j] - gen[j]) for j in batch))
+                dur = (self.ttft if any(not started[j] for j in batch) else 0.0) + self.tpot * tok
+                for j in batch:
+                    if not started[j]:
+                        started[j] = True
+                        first[j] = t
+                batch_of[w], tokens_of[w], free_at[w] = batch, tok, t + dur
+                iters += 1
             host_ms += (time.perf_counter() - h0) * 1e3
-        return StreamResult(first, finish, np.asarray(arrivals_ms, float), iters, gpu_ms / max(iters, 1),
-                            host_ms / max(iters, 1), due_total / max(iters, 1), recorded)
+        return StreamResult(first, finish, np.asarray(arrivals_ms, float), iters, gpu_ms / max(selects, 1),
+                            host_ms / max(selects, 1), due_total / max(selects, 1), recorded)

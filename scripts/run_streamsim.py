@@ -11,7 +11,12 @@ latency.  Random-init weights: the GPU predictor carries no length signal, so it
 the mechanics; "oracle" (true remaining) is the SRTF bound the paper's trained predictor
 approaches.
 
-    python scripts/run_streamsim.py [--n 10000] [--mults 1,3,5] [--config base]
+Workers (W in {1, 8}): per-node Priority Buffers with the
+least-loaded balancer; the arrival rate scales with W (the per-worker rate is the above).
+Priority sources: gpu (random-init BGE predictor), noisy (SPEC NoisyIterative, Laplace error
+with the MAE schedule), oracle (true remaining).  --aging B,A adds starvation control.
+
+    python scripts/run_streamsim.py [--n 10000] [--mults 1,3,5] [--workers 1,8] [--config base]
 """
 import argparse
 import json
@@ -32,7 +37,14 @@ def main():
     ap.add_argument("--config", default="base")
     ap.add_argument("--cap", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--workers", default="1")
+    ap.add_argument("--aging", default="", help="boost_after,boost_amount (e.g. 4,50)")
+    ap.add_argument("--sources", default="fcfs,isrtf_gpu,isrtf_noisy,isrtf_oracle")
     args = ap.parse_args()
+    starv = {}
+    if args.aging:
+        b, a = args.aging.split(",")
+        starv = {"boost_after": int(b), "boost_amount": float(a)}
     import torch
     cfg = inputs.CONFIGS[args.config]
     P = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg, seed=0)), 512 * 64, 64)
@@ -40,22 +52,26 @@ def main():
     lat = inputs.MODEL_AVG_LATENCY_MS["lam13"]
     ttft = 0.05 * lat
     tpot = 0.95 * lat / float(totals.mean())
-    for m in [float(x) for x in args.mults.split(",")]:
-        rate = m * inputs.average_request_rate(lat, args.cap)
-        arr = inputs.arrival_times_ms(args.n, rate, alpha=1.0, seed=args.seed)
-        res = {}
-        for name, policy, source in (("fcfs", 1, "gpu"), ("isrtf_gpu", 0, "gpu"), ("isrtf_oracle", 0, "oracle")):
-            S = StreamSim(P, policy=policy, cap=args.cap, ttft_ms=ttft, tpot_ms=tpot, priority=source)
-            res[name] = S.run(prompts, totals, arr).summary()
-        f = res["fcfs"]["mean_jct_ms"]
-        out = {"config": f"cfg4 stream: {args.n} Poisson requests, rate {m}x ({rate:.4f} req/s), lam13 profile, "
-                         f"cap {args.cap}, K 50, predictor {args.config} on GPU",
-               "rate_multiple": m, "results": res,
-               "isrtf_gpu_vs_fcfs_pct": 100.0 * (res["isrtf_gpu"]["mean_jct_ms"] - f) / f,
-               "isrtf_oracle_vs_fcfs_pct": 100.0 * (res["isrtf_oracle"]["mean_jct_ms"] - f) / f,
-               "paper_context": "up to -19.6% average JCT vs FCFS with the trained predictor on A100 (P:30); "
-                                "11.04 ms average scheduling overhead (P:509)"}
-        print(json.dumps(out), flush=True)
+    table = {"fcfs": (1, "gpu"), "isrtf_gpu": (0, "gpu"), "isrtf_noisy": (0, "noisy"), "isrtf_oracle": (0, "oracle")}
+    for W in [int(x) for x in args.workers.split(",")]:
+        for m in [float(x) for x in args.mults.split(",")]:
+            rate = W * m * inputs.average_request_rate(lat, args.cap)
+            arr = inputs.arrival_times_ms(args.n, rate, alpha=1.0, seed=args.seed)
+            res = {}
+            for name in args.sources.split(","):
+                policy, source = table[name]
+                S = StreamSim(P, policy=policy, cap=args.cap, ttft_ms=ttft, tpot_ms=tpot, priority=source,
+                              workers=W, **starv)
+                res[name] = S.run(prompts, totals, arr).summary()
+            f = res["fcfs"]["mean_jct_ms"]
+            out = {"config": f"cfg4 stream: {args.n} Poisson requests, {W} workers, rate {m}x per worker "
+                             f"({rate:.4f} req/s total), lam13 profile, cap {args.cap}, K 50, predictor {args.config} "
+                             f"on GPU" + (f", aging {starv}" if starv else ""),
+                   "workers": W, "rate_multiple": m, "results": res,
+                   **{f"{k}_vs_fcfs_pct": 100.0 * (v["mean_jct_ms"] - f) / f for k, v in res.items() if k != "fcfs"},
+                   "paper_context": "up to -19.6% average JCT vs FCFS with the trained predictor on A100 (P:30); "
+                                    "11.04 ms average scheduling overhead (P:509)"}
+            print(json.dumps(out), flush=True)
     P.close()
     del torch
 

@@ -30,10 +30,14 @@ def make_stream(n, mult, seed):
     return prompts, totals, arr, 0.05 * inputs.MODEL_AVG_LATENCY_MS["lam13"], tpot
 
 
-def replay(totals, arr, policy, cap, ttft, tpot, allow, priority):
-    from oracle import sim
+def replay(totals, arr, policy, cap, ttft, tpot, allow, priority, workers=1, **starv):
+    from oracle import scheduler, sim
     jobs = [sim.SimJob(i, float(arr[i]), int(totals[i])) for i in range(len(totals))]
-    r = sim.simulate(jobs, policy, cap=cap, K=50, ttft=ttft, tpot=tpot, allow_preempt=allow, priority=priority)
+    if workers == 1 and not starv:
+        r = sim.simulate(jobs, policy, cap=cap, K=50, ttft=ttft, tpot=tpot, allow_preempt=allow, priority=priority)
+    else:
+        r = scheduler.simulate_nodes(jobs, workers, policy, cap=cap, K=50, ttft=ttft, tpot=tpot,
+                                     allow_preempt=allow, priority=priority, **starv)
     return np.array([r[i][0] for i in range(len(jobs))]), np.array([r[i][1] for i in range(len(jobs))])
 
 
@@ -64,3 +68,33 @@ def test_srtf_beats_fcfs_on_the_stream(tiny_predictor):
     s = StreamSim(tiny_predictor, policy=0, cap=4, ttft_ms=ttft, tpot_ms=tpot, priority="oracle").run(
         prompts, totals, arr)
     assert s.jct.mean() < f.jct.mean()
+
+
+@pytest.mark.parametrize("workers,source,starv", [
+    (3, "gpu", {}), (3, "oracle", {}), (8, "gpu", {"boost_after": 2, "boost_amount": 40.0}),
+    (1, "gpu", {"boost_after": 1, "boost_amount": 25.0, "preempt_margin": 10.0}),
+    (4, "oracle", {"preempt_margin": 30.0})])
+def test_multi_worker_stream_matches_oracle_replay(tiny_predictor, workers, source, starv):
+    """Per-node Priority Buffers + least-loaded balancer + starvation control on the GPU
+     replayed through oracle/scheduler.simulate_nodes."""
+    from oracle import sim
+    from paper_2505_09142_b200.streamsim import StreamSim
+    prompts, totals, arr, ttft, tpot = make_stream(160, 3.0 * workers, seed=3 + workers)
+    S = StreamSim(tiny_predictor, policy=0, cap=4, ttft_ms=ttft, tpot_ms=tpot, priority=source,
+                  workers=workers, **starv)
+    res = S.run(prompts, totals, arr)
+    assert np.isfinite(res.finish).all() and (res.finish >= res.first).all()
+    prio = (lambda job, g: res.recorded[(job.id, g)]) if source == "gpu" else sim.oracle_remaining
+    first, finish = replay(totals, arr, 0, 4, ttft, tpot, True, prio, workers, **starv)
+    np.testing.assert_array_equal(res.first, first)
+    np.testing.assert_array_equal(res.finish, finish)
+
+
+def test_fcfs_multi_worker_matches_oracle(tiny_predictor):
+    from oracle import sim
+    from paper_2505_09142_b200.streamsim import StreamSim
+    prompts, totals, arr, ttft, tpot = make_stream(140, 6.0, seed=11)
+    res = StreamSim(tiny_predictor, policy=1, cap=2, ttft_ms=ttft, tpot_ms=tpot, workers=5).run(prompts, totals, arr)
+    first, finish = replay(totals, arr, 1, 2, ttft, tpot, True, sim.oracle_remaining, 5)
+    np.testing.assert_array_equal(res.first, first)
+    np.testing.assert_array_equal(res.finish, finish)

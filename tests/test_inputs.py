@@ -49,3 +49,20 @@ def test_weights_bf16_representable_and_count():
     assert flat.size == inputs.weight_count(cfg)
     enc = flat[: flat.size - sum(int(np.prod(s)) for n, s in inputs.weight_shapes(cfg) if n.startswith("head."))]
     np.testing.assert_array_equal(inputs.round_to_bf16(enc), enc)
+
+
+def test_noisy_remaining_spec():
+    """max(0, total + e - generated), e ~ Laplace(MAE of the step), seeded
+    per (job, step): deterministic, error MAE per step equals the schedule (Laplace mean absolute
+    deviation = scale), non-increasing with the step."""
+    a = inputs.noisy_remaining(7, 120, 100, seed=3)
+    assert a == inputs.noisy_remaining(7, 120, 100, seed=3) and a >= 0.0
+    maes = []
+    for step in range(7):
+        g = 50 * step
+        err = np.array([inputs.noisy_remaining(j, 100000, g) - (100000 - g) for j in range(4000)])
+        maes.append(np.abs(err).mean())
+        want = inputs.NOISY_MAE_SCHEDULE[min(step, 5)]
+        assert abs(maes[-1] - want) < 0.06 * want
+    assert all(maes[i + 1] <= maes[i] * 1.05 for i in range(6))
+    assert inputs.noisy_remaining(1, 10, 10) >= 0.0
