@@ -83,6 +83,21 @@ struct SmemPlan {
 // 2.6e-5 (scripts/fit_gelu.py), < 1/75 of the bf16 rounding of the output this epilogue
 // writes.  10 instructions incl. 2 MUFU instead of ~28 for erff (the FFN1 epilogue is
 // instruction-issue bound).
+#ifdef ELIS_GELU_TANH
+// Same minimax sigmoid form evaluated as x sigmoid(y) = 0.5 x (1 + tanh(y / 2)): one MUFU
+// (tanh.approx) instead of two; error measured by scripts/gelu_acc.cu.
+ELIS_DEV float gelu_fast(float x) {
+  constexpr float a0 = 0.5f * 1.5950205882421884f, a1 = 0.5f * 0.07400664121448398f,
+                  a2 = -0.5f * 0.0007022165804436097f;
+  const float xc = fminf(fmaxf(x, -9.0f), 9.0f);
+  const float x2 = xc * xc;
+  const float q = fmaf(fmaf(a2, x2, a1), x2, a0);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(xc * q));
+  const float h = 0.5f * x;
+  return fmaf(h, t, h);
+}
+#else
 ELIS_DEV float gelu_fast(float x) {
   constexpr float kL2E = 1.4426950408889634f;
   constexpr float c0 = -1.5950205882421884f * kL2E, c1 = -0.07400664121448398f * kL2E,
@@ -95,6 +110,7 @@ ELIS_DEV float gelu_fast(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
   return x * r;
 }
+#endif
 
 // Chan et al. merge of (count, mean, M2) partial statistics.
 ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
