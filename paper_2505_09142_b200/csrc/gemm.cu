@@ -37,6 +37,21 @@
 
 namespace elis {
 
+#ifdef ELIS_GEMM_TRACE
+// Diagnostic build only (--variant=gtrace -DELIS_GEMM_TRACE): per-CTA clock64 totals of the
+// GEMM roles' waits, overwritten by every launch.  Slots: 0 producer wait(empty), 1 MMA
+// wait(tempty), 2 MMA wait(full), 3 MMA busy span, 4 epi wait(tfull), 5 epi pass 1,
+// 6 epi wait(stats), 7 epi pass 2, 8 epi total span, 9 tiles, 10 smid.
+constexpr int kGemmTraceCtas = 1024;
+__device__ long long g_gemm_trace[kGemmTraceCtas * 16];
+#define GT_ADD(slot, v) \
+  do { if (blockIdx.x < kGemmTraceCtas) g_gemm_trace[blockIdx.x * 16 + (slot)] += (v); } while (0)
+#define GT_CLK() clock64()
+#else
+#define GT_ADD(slot, v) do { } while (0)
+#define GT_CLK() 0ll
+#endif
+
 namespace {
 
 constexpr int BM = 128;  // rows per CTA (256 per pair)
@@ -208,7 +223,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int m, n;
         tile_mn(t, m, n);
         for (int kb = 0; kb < num_k; ++kb) {
+          const long long g0 = GT_CLK();
           mbar_wait(&empty[s], ph ^ 1u);
+          GT_ADD(0, GT_CLK() - g0);
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
           const uint32_t bar = mapa_shared(smem_u32(&full[s]), leader_rank);
           tma_load_2d_pair(sA + s * C::A_BYTES, &tmA, bar, kb * BK, m * 2 * BM + hrow * BM);
@@ -225,14 +242,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
+      const long long gstart = GT_CLK();
       for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
+        long long g0 = GT_CLK();
         mbar_wait_acquire_cluster(&tempty[acc], aph ^ 1u);
+        GT_ADD(1, GT_CLK() - g0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_k; ++kb) {
+          g0 = GT_CLK();
           mbar_wait(&full[s], ph);
+          GT_ADD(2, GT_CLK() - g0);
           tc_fence_after();
           const uint64_t da = make_sw128_desc(smem_u32(sA + s * C::A_BYTES));
           const uint64_t db = make_sw128_desc(smem_u32(sB + s * C::B_BYTES));
@@ -246,6 +268,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         tc_commit_pair_mc(&tfull[acc], mask);
       }
+      GT_ADD(3, GT_CLK() - gstart);
+      GT_ADD(9, it);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (each CTA: its 128 rows; warp: 32 rows x BN/2 columns)
@@ -304,6 +328,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       named_bar_sync(1, kEpiWarps * 32);
     }
     int it = 0;
+    const long long gepi = GT_CLK();
     bool res_prefetched = false;  // LN: the next tile's first residual boxes were issued early
     for (int t = cid; t < num_iter_tiles; t += ncl, ++it) {
       int m, n;
@@ -322,7 +347,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         stage_vectors(n);
         named_bar_sync(1, kEpiWarps * 32);
       }
+      const bool gt_me = (warp == 4 && lane == 0);
+      long long g0 = GT_CLK();
       mbar_wait(&tfull[acc], aph);
+      long long g1 = GT_CLK();
+      if (gt_me) GT_ADD(4, g1 - g0);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + cbase;
       float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // LN row statistics over this warp's columns
@@ -392,6 +421,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           issue_store(b, row0, col0);
         }
       }
+      if (gt_me) { const long long g2 = GT_CLK(); GT_ADD(5, g2 - g1); g1 = g2; }
       if constexpr (LN) {
         tc_wait_st();
         // pass 1 has consumed this tile's residual: start the next tile's first boxes now so the
@@ -424,6 +454,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (lane == 0) mbar_wait_acquire_cluster(&sfull[slot], sph);
         __syncwarp();
+        if (gt_me) { const long long g2 = GT_CLK(); GT_ADD(6, g2 - g1); g1 = g2; }
         // merge the cpairs partials in pair order (identical on every CTA) -> mean, rstd
         float tn = 0.f, tmean = 0.f, tm2 = 0.f;
         for (int p = 0; p < cpairs; ++p) {
@@ -462,6 +493,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                            pack_bf16x2(y[8 * k + 4], y[8 * k + 5]), pack_bf16x2(y[8 * k + 6], y[8 * k + 7]));
           issue_store(b, row0, col0);
         }
+        if (gt_me) GT_ADD(7, GT_CLK() - g1);
       }
       tc_fence_before();
       __syncwarp();
@@ -469,6 +501,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) mbar_arrive_remote_relaxed(tempty_leader + acc * 8);
     }
     if (lane == 0) tma_store_wait_all<0>();
+    if (warp == 4 && lane == 0) {
+      GT_ADD(8, GT_CLK() - gepi);
+#ifdef ELIS_GEMM_TRACE
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      if (blockIdx.x < kGemmTraceCtas) g_gemm_trace[blockIdx.x * 16 + 10] = smid;
+#endif
+    }
   }
   tc_fence_before();
   cluster_sync_all();
@@ -651,5 +691,16 @@ bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const flo
   return make_tmap_2d(&g->tmOb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, outb, rows, g->args.N, kBox, kBox,
                       CU_TENSOR_MAP_SWIZZLE_64B);
 }
+
+#ifdef ELIS_GEMM_TRACE
+extern "C" int elis_debug_gemm_trace(long long* host, size_t n, int reset) {
+  if (reset) {
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_gemm_trace);
+    return static_cast<int>(cudaMemset(p, 0, sizeof(g_gemm_trace)));
+  }
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_gemm_trace, (n < kGemmTraceCtas * 16 ? n : kGemmTraceCtas * 16) * 8));
+}
+#endif
 
 }  // namespace elis
