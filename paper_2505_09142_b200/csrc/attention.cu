@@ -279,6 +279,33 @@ ELIS_DEV float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// exp2 of a pair on the FMA pipe, to take part of the softmax exponentials off the MUFU
+// (16 ex2 / clk / SM, the softmax bound when 4 CTAs share an SM):
+//   j = rint(x) (x + 1.5 * 2^23 leaves j in the low mantissa bits), f = x - j in [-1/2, 1/2],
+//   2^f = degree-3 minimax polynomial (max relative error 7.5e-5, scripts/fit_exp2.py; P is then
+//   rounded to bf16, relative step 3.9e-3), 2^x = bits(2^f) + (j << 23).
+// x is clamped at -125 so the exponent stays normal (the true value is then < 2^-125 next to the
+// row maximum's 1).
+#ifndef ELIS_EXP2_POLY
+#define ELIS_EXP2_POLY 6  // pairs of every 16 in a 32-key chunk evaluated by exp2_poly2
+#endif
+ELIS_DEV unsigned long long exp2_poly2(float x0, float x1) {
+  const unsigned long long xx = f2_pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const unsigned long long t = f2_add(xx, f2_pack(12582912.f, 12582912.f));
+  const unsigned long long j = f2_add(t, f2_pack(-12582912.f, -12582912.f));
+  const unsigned long long f = f2_fma(j, f2_pack(-1.f, -1.f), xx);
+  unsigned long long p = f2_fma(f2_pack(0.0551716685f, 0.0551716685f), f, f2_pack(0.2426111251f, 0.2426111251f));
+  p = f2_fma(p, f, f2_pack(0.6932609677f, 0.6932609677f));
+  p = f2_fma(p, f, f2_pack(0.9999280572f, 0.9999280572f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  return f2_pack(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23)),
+                 __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23)));
+}
+ELIS_DEV constexpr bool exp2_on_fma(int pair) {
+  return ((pair + 1) * ELIS_EXP2_POLY) / 16 != (pair * ELIS_EXP2_POLY) / 16;  // spread over the chunk
+}
 
 __global__ void __launch_bounds__(128, 4)
     k_attention_tc(const __grid_constant__ CUtensorMap tm,
@@ -327,7 +354,7 @@ __global__ void __launch_bounds__(128, 4)
     mbar_arrive_expect_tx(v_full, kBlkBytes);
     tma_load_2d(sV, &tm, v_full, 0, (2 * nh + h) * Tp + start);
   }
-  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  if (warp == 1) tmem_alloc<128>(tmem_slot);  // warp 0's thread 0 is issuing the loads
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -409,8 +436,12 @@ __global__ void __launch_bounds__(128, 4)
         for (int e = 0; e < 16; ++e) {
           float x0, x1;
           f2_unpack(f2_fma(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
-          p[2 * e] = ex2_approx(x0);
-          p[2 * e + 1] = ex2_approx(x1);
+          if (exp2_on_fma(e)) {
+            f2_unpack(exp2_poly2(x0, x1), p[2 * e], p[2 * e + 1]);
+          } else {
+            p[2 * e] = ex2_approx(x0);
+            p[2 * e + 1] = ex2_approx(x1);
+          }
         }
         if (nv < 32) {
 #pragma unroll
@@ -470,25 +501,36 @@ __global__ void __launch_bounds__(128, 4)
     __syncthreads();  // every row has read O_j before the next S MMA overwrites columns [0, 128)
     if (j == 0) ATTN_TRACE(5, attn_gtime());
   }
-  // epilogue: ctx = O / l (bf16)
-  if (q0 + row < L) {
+  // epilogue: ctx = O / l (bf16).  Rows are staged in shared memory (sQ: the last S MMA has
+  // completed) with 16-byte chunks XOR-swizzled by row, then written back 4 rows per warp
+  // instruction, each row one contiguous 128-byte line (thread-per-row stores would touch 32
+  // lines per instruction).
+  {
     const float inv = 1.0f / l;
-    uint4* dst = reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + row) * H + h * TD);
     float o[TD];
 #pragma unroll
     for (int i = 0; i < TD / 2; ++i) f2_unpack(o2[i], o[2 * i], o[2 * i + 1]);
+    uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      dst[k] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
-                          pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
-                          pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
-                          pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
+      srow[k ^ (row & 7)] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
+                                       pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
+                                       pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
+                                       pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<128>(tmem);
+  }
+  {
+    const int nrows = min(TQ, L - q0);
+    const int c = lane & 7;
+    for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
+      const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
+      *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+    }
   }
 #ifdef ELIS_ATTN_TRACE
   ATTN_TRACE(6, attn_gtime());

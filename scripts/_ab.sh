@@ -1,0 +1,4 @@
+# A/B: per-kernel ms of the BGE-base cfg2 predict for each library given as argument
+for v in "$@"; do
+  echo "== $v"; ELIS_LIB=$v timeout 120 python scripts/run_predict.py --time --iters 30 2>&1 | head -1
+done
