@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--lengths", default="trace", help="trace | uniform | fixed:L")
     ap.add_argument("--cap", type=int, default=4, help="batch_cap")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--precision", choices=["bf16", "fp8"], default="bf16",
+                    help="encoder GEMM operands: bf16 (default, the parity-bound path) or fp8 E4M3 "
+                         "(SURVEY.md 8f row f4(i); looser tolerance, DESIGN.md R20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=12, help="requests in the oracle sample")
     ap.add_argument("--inflight", type=int, default=0,
@@ -92,6 +95,7 @@ def config_desc(args, T_local, world):
         "lengths": args.lengths,
         "batch_cap": args.cap,
         "pooling": "mean",
+        "precision": args.precision,
         "parallelism": f"request-sharded dp{world}" if world > 1 else "single GPU",
         "l2": "no flush: per-step working set (218 MB bf16 weights + >=0.5 GB activations) exceeds the 126 MB L2",
     }
@@ -172,7 +176,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- roofline
-def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic_table: dict):
+def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic_table: dict, fp8: bool = False):
     """Dominant kernel class (largest share of device time) -> achieved vs measured peak."""
     H, F, nl = cfg.hidden, cfg.intermediate, cfg.num_layers
     flops = {  # algorithmic FLOPs per launch
@@ -193,6 +197,8 @@ def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic
         achieved = flops[name] / avg_s / 1e12
         peak = peaks.get("bf16_tflops_sustained") or 1400.0
         peak_src = "measured sustained bf16 (MEASURED_PEAKS.json)" if peaks.get("bf16_tflops_sustained") else "fallback"
+        if fp8 and name.startswith("gemm"):   # E4M3 operands: the bf16 peak x the nominal fp8/bf16 ratio 2
+            peak, peak_src = 2.0 * peak, peak_src + " x 2 (nominal fp8/bf16 dense ratio)"
     else:
         bound, unit = "hbm", "GB/s"
         achieved = bytes_.get(name, 0.0) / avg_s / 1e9
@@ -322,7 +328,7 @@ def run_elis(args):
         L = windows[0][5]
         tokens = windows[0][4]
         gen = gen_t[:n]
-        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local)
+        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision)
         d_table = torch.zeros(F, device="cuda")
         d_gen = torch.from_numpy(gen_t).cuda()
         for wt in windows:  # fill every slot's cached prediction once
@@ -341,7 +347,7 @@ def run_elis(args):
         L, gen, tokens = workload(args, rank)
         n, T = len(L), int(L.sum())
         T_roof = T
-        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local)
+        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision)
         d_tok = torch.from_numpy(tokens).cuda()
         d_len = torch.from_numpy(L).cuda()
         d_gen = torch.from_numpy(gen).cuda()
@@ -437,12 +443,14 @@ def run_elis(args):
     out = None
     if rank == 0:
         peaks = load_peaks()
-        roof = kernel_roofline(prof, cfg, T_roof, L, peaks, load_traffic())
+        roof = kernel_roofline(prof, cfg, T_roof, L, peaks, load_traffic() if args.precision == "bf16" else {},
+                               fp8=args.precision == "fp8")
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "ms_per_step_p10_p50_p90": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90)],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.precision == "bf16" else "fp8_e4m3 GEMMs (bf16 attention, fp32 residual/LN/head)",
             "data": "synthetic (seeded trace-shaped lengths, uniform token ids, random-init BGE weights)",
             "config": config_desc(args, T_roof, world),
             "tokens_per_s": round(world * T * args.steps / (total_ms / 1e3), 1),

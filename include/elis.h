@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define ELIS_ABI_VERSION 2
+#define ELIS_ABI_VERSION 3
 
 typedef enum {
   ELIS_OK = 0,
@@ -55,6 +55,13 @@ typedef enum {
 
 typedef enum { ELIS_POOL_MEAN = 0, ELIS_POOL_CLS = 1 } elis_pooling;   /* P:359 / P:138 */
 typedef enum { ELIS_POLICY_ISRTF = 0, ELIS_POLICY_FCFS = 1 } elis_policy; /* P:22 / P:463 */
+/* Operand precision of the encoder GEMMs (the paper never states one, R12).
+ * BF16: bf16 operands, fp32 accumulate (the parity-bound default).
+ * FP8:  E4M3 weights (per-output-channel scale) and E4M3 activations (static power-of-two
+ *       scales) on tcgen05 kind::f8f6f4, fp32 accumulate; attention stays bf16, the residual
+ *       stream / LayerNorm / head stay fp32 (R20).
+ *       Requires head dim 64 and hidden, intermediate multiples of 256 (BGE-base / large). */
+typedef enum { ELIS_PREC_BF16 = 0, ELIS_PREC_FP8 = 1 } elis_precision;
 
 /* Encoder + head shape.  BGE-base = {30522, 512, 2, 12, 768, 12, 3072}
  * (P:121, P:123 [Sec. 3.1]); head = 8 layers, hidden 1024. */
@@ -75,6 +82,7 @@ typedef struct {
   int32_t max_tokens;         /* workspace capacity: max sum(lengths) per predict call        */
   int32_t max_requests;       /* workspace capacity: max n per predict / select call          */
   int32_t device;             /* CUDA device ordinal                                          */
+  int32_t precision;          /* elis_precision; default BF16                                 */
 } elis_config;
 
 typedef struct elis_predictor elis_predictor;

@@ -33,6 +33,25 @@ elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* b
                             const float* gamma, const float* beta, float eps, uint16_t* outb, int32_t M, int32_t N,
                             int32_t K, void* stream);
 
+/* FP8 weight preparation (R20): W f32 [rows, cols]
+ * (cols % 4 == 0) -> q E4M3 bytes [rows, cols] = RNE-saturate(W[r, :] * 448 / amax_r) and
+ * scale f32 [rows] = amax_r / 448 * post (1 * post for an all-zero row). */
+elis_status elis_op_quant_rows_e4m3(const float* W, int32_t rows, int32_t cols, uint8_t* q, float* scale, float post,
+                                   void* stream);
+
+/* tcgen05 kind::f8f6f4 GEMM: A, W E4M3 bytes [M, K] / [N, K] row-major, fp32 accumulate;
+ * v = (A W^T)[m, n] * colscale[n] + bias[n].  epilogue ELIS_EPI_BIAS_BF16: out bf16 [M, N] = v;
+ * ELIS_EPI_BIAS_GELU_BF16: out E4M3 bytes [M, N] = E4M3(out_scale * GELU(v)).
+ * N % 256 == 0, K % 128 == 0. */
+elis_status elis_op_gemm_f8(const uint8_t* A, const uint8_t* W, const float* colscale, const float* bias, void* out,
+                            int32_t M, int32_t N, int32_t K, int32_t epilogue, float out_scale, void* stream);
+
+/* FP8 variant of elis_op_gemm_ln: v = (A W^T) colscale + bias + resid_inout; resid_inout <- LN(v)
+ * (fp32, in place), outb E4M3 bytes [M, N] = E4M3(out_scale * LN(v)).  N in {256, 512, 768, 1024}. */
+elis_status elis_op_gemm_ln_f8(const uint8_t* A, const uint8_t* W, const float* colscale, const float* bias,
+                               float* resid_inout, const float* gamma, const float* beta, float eps, uint8_t* outb,
+                               float out_scale, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* Varlen bidirectional multi-head attention ("process tokens in parallel").
  * d = 64: qkv bf16 head-major planes [3 * num_heads][T][64] (plane h = Q of head h, plane
  *         num_heads + h = K, plane 2 num_heads + h = V) -- the layout the QKV GEMM writes;

@@ -19,11 +19,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 
 ELIS_OK = 0
-ABI_VERSION = 2  # include/elis.h ELIS_ABI_VERSION
+ABI_VERSION = 3  # include/elis.h ELIS_ABI_VERSION
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
           6: "nccl", 7: "device input"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
 EPI_BIAS_BF16, EPI_BIAS_GELU_BF16, EPI_BIAS_RESID_F32 = 0, 1, 2
+PRECISION = {"bf16": 0, "fp8": 1}  # elis_precision
 
 _vp, _i32, _i64, _u32, _f32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
                                     ctypes.c_float, ctypes.c_size_t)
@@ -33,7 +34,8 @@ class ElisConfig(ctypes.Structure):
     _fields_ = [("abi_version", _i32), ("vocab_size", _i32), ("max_position", _i32), ("type_vocab_size", _i32),
                 ("num_layers", _i32), ("hidden", _i32), ("num_heads", _i32), ("intermediate", _i32),
                 ("ln_eps", _f32), ("pooling", _i32), ("head_layers", _i32), ("head_hidden", _i32),
-                ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32)]
+                ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32),
+                ("precision", _i32)]
 
 
 class ElisStarvation(ctypes.Structure):
@@ -98,6 +100,9 @@ def lib():
         "elis_profile_read": (_i32, [_vp, _vp, _vp, _vp, _i32]),
         "elis_op_gemm": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
         "elis_op_gemm_ln": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _i32, _i32, _i32, _vp]),
+        "elis_op_quant_rows_e4m3": (_i32, [_vp, _i32, _i32, _vp, _vp, _f32, _vp]),
+        "elis_op_gemm_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32, _vp]),
+        "elis_op_gemm_ln_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _f32, _i32, _i32, _i32, _vp]),
         "elis_op_attention": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
         "elis_op_layernorm": (_i32, [_vp, _vp, _vp, _f32, _i64, _i32, _vp, _vp, _vp]),
         "elis_op_fc_f32": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
@@ -135,20 +140,21 @@ def _stream(stream):
 
 
 def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
-                head_predicts_total: bool = False) -> ElisConfig:
+                head_predicts_total: bool = False, precision: str = "bf16") -> ElisConfig:
     return ElisConfig(ABI_VERSION, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
                       cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
-                      int(head_predicts_total), int(max_tokens), int(max_requests), int(device))
+                      int(head_predicts_total), int(max_tokens), int(max_requests), int(device), PRECISION[precision])
 
 
 class Predictor:
     """Owner of one elis_predictor (device weights + workspaces)."""
 
     def __init__(self, cfg: inputs.EncoderConfig, flat_weights: np.ndarray, max_tokens: int, max_requests: int,
-                 device: int = 0, head_predicts_total: bool = False):
+                 device: int = 0, head_predicts_total: bool = False, precision: str = "bf16"):
         L = lib()
         self.cfg = cfg
-        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total)
+        self.precision = precision
+        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total, precision)
         flat = np.ascontiguousarray(flat_weights, dtype=np.float32)
         need = L.elis_weight_count(ctypes.byref(self.c))
         if need != flat.size:
@@ -268,6 +274,27 @@ def op_gemm_ln(A, W, bias, resid_inout, gamma, beta, eps: float, outb, stream=No
     N = W.shape[0]
     check(lib().elis_op_gemm_ln(_ptr(A), _ptr(W), _ptr(bias), _ptr(resid_inout), _ptr(gamma), _ptr(beta), eps,
                                 _ptr(outb), M, N, K, _stream(stream)), "elis_op_gemm_ln")
+
+
+def op_quant_rows_e4m3(W, q, scale, post: float = 1.0, stream=None):
+    rows, cols = W.shape
+    check(lib().elis_op_quant_rows_e4m3(_ptr(W), rows, cols, _ptr(q), _ptr(scale), post, _stream(stream)),
+          "elis_op_quant_rows_e4m3")
+
+
+def op_gemm_f8(A, W, colscale, bias, out, epilogue: int, out_scale: float = 1.0, stream=None):
+    M, K = A.shape
+    N = W.shape[0]
+    check(lib().elis_op_gemm_f8(_ptr(A), _ptr(W), _ptr(colscale), _ptr(bias), _ptr(out), M, N, K, epilogue,
+                                out_scale, _stream(stream)), "elis_op_gemm_f8")
+
+
+def op_gemm_ln_f8(A, W, colscale, bias, resid_inout, gamma, beta, eps: float, outb, out_scale: float, stream=None):
+    M, K = A.shape
+    N = W.shape[0]
+    check(lib().elis_op_gemm_ln_f8(_ptr(A), _ptr(W), _ptr(colscale), _ptr(bias), _ptr(resid_inout), _ptr(gamma),
+                                   _ptr(beta), eps, _ptr(outb), out_scale, M, N, K, _stream(stream)),
+          "elis_op_gemm_ln_f8")
 
 
 def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None):

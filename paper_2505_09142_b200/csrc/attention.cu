@@ -307,10 +307,12 @@ ELIS_DEV constexpr bool exp2_on_fma(int pair) {
   return ((pair + 1) * ELIS_EXP2_POLY) / 16 != (pair * ELIS_EXP2_POLY) / 16;  // spread over the chunk
 }
 
+// F8OUT: ctx written as E4M3(ctx_scale * ctx) bytes [T, H] (the FP8 out-projection's A operand)
+template <bool F8OUT>
 __global__ void __launch_bounds__(128, 4)
     k_attention_tc(const __grid_constant__ CUtensorMap tm,
                    const AttnWork* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
-                   uint16_t* __restrict__ ctx, float scale_log2, int Tp) {
+                   uint16_t* __restrict__ ctx, float scale_log2, int Tp, float ctx_scale) {
 #ifdef ELIS_ATTN_TRACE
   const unsigned long long t_start = attn_gtime();
 #endif
@@ -506,17 +508,30 @@ __global__ void __launch_bounds__(128, 4)
   // instruction, each row one contiguous 128-byte line (thread-per-row stores would touch 32
   // lines per instruction).
   {
-    const float inv = 1.0f / l;
     float o[TD];
 #pragma unroll
     for (int i = 0; i < TD / 2; ++i) f2_unpack(o2[i], o[2 * i], o[2 * i + 1]);
-    uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
+    if constexpr (F8OUT) {  // 64-byte rows: 4 pieces, XOR-swizzled by row & 3
+      const float inv = ctx_scale / l;
+      uint4* srow = reinterpret_cast<uint4*>(sQ + row * TD);
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      srow[k ^ (row & 7)] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
-                                       pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
-                                       pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
-                                       pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
+      for (int k = 0; k < 4; ++k)
+        srow[k ^ (row & 3)] =
+            make_uint4(pack_e4m3x4(o[16 * k + 0] * inv, o[16 * k + 1] * inv, o[16 * k + 2] * inv, o[16 * k + 3] * inv),
+                       pack_e4m3x4(o[16 * k + 4] * inv, o[16 * k + 5] * inv, o[16 * k + 6] * inv, o[16 * k + 7] * inv),
+                       pack_e4m3x4(o[16 * k + 8] * inv, o[16 * k + 9] * inv, o[16 * k + 10] * inv, o[16 * k + 11] * inv),
+                       pack_e4m3x4(o[16 * k + 12] * inv, o[16 * k + 13] * inv, o[16 * k + 14] * inv,
+                                   o[16 * k + 15] * inv));
+    } else {
+      const float inv = 1.0f / l;
+      uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        srow[k ^ (row & 7)] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
+                                         pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
+                                         pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
+                                         pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -526,10 +541,19 @@ __global__ void __launch_bounds__(128, 4)
   }
   {
     const int nrows = min(TQ, L - q0);
-    const int c = lane & 7;
-    for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
-      const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
-      *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+    if constexpr (F8OUT) {
+      uint8_t* c8 = reinterpret_cast<uint8_t*>(ctx);
+      const int c = lane & 3;
+      for (int rr = warp * 8 + (lane >> 2); rr < nrows; rr += 32) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * TD)[c ^ (rr & 3)];
+        *reinterpret_cast<uint4*>(c8 + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 16) = v;
+      }
+    } else {
+      const int c = lane & 7;
+      for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
+        *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+      }
     }
   }
 #ifdef ELIS_ATTN_TRACE
@@ -549,7 +573,7 @@ bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, cudaStream_t st) {
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, cudaStream_t st) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
@@ -557,11 +581,13 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
   const unsigned grid = static_cast<unsigned>(max_tiles * num_heads);
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
+    auto kern = ctx_f8_scale > 0.f ? k_attention_tc<true> : k_attention_tc<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
     if (e != cudaSuccess) return e;
-    k_attention_tc<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
-                                                   static_cast<int>(plane_rows));
+    kern<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
+                                         static_cast<int>(plane_rows), ctx_f8_scale);
   } else if (d == 32) {
+    if (ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, num_heads, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;

@@ -29,6 +29,11 @@ ELIS_DEV float bf16_bits_to_f32(uint16_t b) {
 ELIS_DEV int warp_id() { return threadIdx.x >> 5; }
 ELIS_DEV int lane_id() { return threadIdx.x & 31; }
 
+ELIS_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 ELIS_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -177,6 +182,17 @@ ELIS_DEV void tc_mma_f16_pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b,
       "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// kind::f8f6f4 (E4M3 x E4M3, fp32 accumulate; 32 bytes = 32 elements of K per instruction).
+ELIS_DEV void tc_mma_f8_pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive (multicast) on the barrier at the same offset in every CTA of `cta_mask`.
 ELIS_DEV void tc_commit_pair_mc(uint64_t* bar, uint16_t cta_mask) {
   asm volatile(
@@ -313,6 +329,19 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(uint32_t M, uint32_t 
          | (1u << 10)           // B format bf16
          | ((N >> 3) << 17)     // N >> 3
          | ((M >> 4) << 24);    // M >> 4
+}
+
+// Instruction descriptor, kind::f8f6f4: D f32, A/B E4M3 (format 0), both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t make_idesc_e4m3_f32(uint32_t M, uint32_t N) {
+  return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// Four fp32 -> four E4M3 bytes (round to nearest even, saturating to +-448), x0 in the low byte.
+ELIS_DEV uint32_t pack_e4m3x4(float x0, float x1, float x2, float x3) {
+  uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(x1), "f"(x0));  // a -> upper byte
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(x3), "f"(x2));
+  return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
 }
 
 }  // namespace elis

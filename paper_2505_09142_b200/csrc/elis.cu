@@ -92,6 +92,9 @@ bool config_valid(const elis_config* c, std::string* why) {
   if (c->pooling != ELIS_POOL_MEAN && c->pooling != ELIS_POOL_CLS) return bad("pooling");
   if (c->head_layers < 2 || c->head_hidden < 1) return bad("head_layers >= 2, head_hidden >= 1");
   if (c->max_tokens < 1 || c->max_requests < 1) return bad("max_tokens / max_requests must be >= 1");
+  if (c->precision != ELIS_PREC_BF16 && c->precision != ELIS_PREC_FP8) return bad("precision");
+  if (c->precision == ELIS_PREC_FP8 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
+    return bad("FP8 needs head dim 64 and hidden, intermediate multiples of 256");
   return true;
 }
 
@@ -108,8 +111,16 @@ size_t weight_count_impl(const elis_config* c) {
   return n;
 }
 
+// Static power-of-two scales of the FP8 activations (R20): the stored byte is
+// E4M3(scale * value).  LayerNorm outputs |y| <= sqrt(H - 1) max|gamma| + max|beta| (~30 for BERT);
+// attention outputs are convex combinations of V rows; GELU outputs of the FFN1 projection.
+constexpr float kF8ScaleHidden = 8.f;   // hb: saturates at |y| = 56
+constexpr float kF8ScaleCtx = 16.f;     // ctx: saturates at 28
+constexpr float kF8ScaleGelu = 16.f;    // g: saturates at 28
+
 struct Layer {
-  uint16_t *wqkv, *wo, *w1, *w2;
+  uint16_t *wqkv, *wo, *w1, *w2;   // bf16, or E4M3 bytes (same allocation) in FP8 mode
+  float *sqkv = nullptr, *so = nullptr, *s1 = nullptr, *s2 = nullptr;  // FP8: per-output-channel dequant
   float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
   GemmPlan p_qkv, p_out, p_ffn1, p_ffn2;
 };
@@ -304,6 +315,17 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   auto up_f32 = [&](float* dst, const float* src, size_t n) {
     return cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice);
   };
+  const bool f8 = cfg->precision == ELIS_PREC_FP8;
+  float* wtmp = nullptr;  // FP8: fp32 staging of one matrix for the on-device quantiser
+  if (f8 && p->alloc(&wtmp, static_cast<size_t>(F) * H) != cudaSuccess) return cleanup_fail(ELIS_ERR_OOM, "cudaMalloc wtmp");
+  // encoder matrix [rows, cols] -> bf16, or E4M3 + per-row scale (x post) in FP8 mode
+  auto up_mat = [&](uint16_t* dst, const float* src, int rows, int cols, float* sdst, float post) {
+    if (!f8) return up_bf16(dst, src, static_cast<size_t>(rows) * cols);
+    cudaError_t e = up_f32(wtmp, src, static_cast<size_t>(rows) * cols);
+    if (e != cudaSuccess) return e;
+    e = launch_quant_rows_e4m3(wtmp, rows, cols, reinterpret_cast<uint8_t*>(dst), sdst, post, nullptr);
+    return e != cudaSuccess ? e : cudaDeviceSynchronize();
+  };
   ALLOC(p->word, static_cast<size_t>(V) * H);
   ALLOC(p->pos, static_cast<size_t>(P) * H);
   ALLOC(p->type0, H);
@@ -334,19 +356,26 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     ALLOC(L.b2, H);
     ALLOC(L.ln2g, H);
     ALLOC(L.ln2b, H);
+    if (f8) {
+      ALLOC(L.sqkv, 3 * H);
+      ALLOC(L.so, H);
+      ALLOC(L.s1, F);
+      ALLOC(L.s2, H);
+    }
     bool ok = true;
     for (int j = 0; j < 3; ++j) {  // query, key, value -> rows [jH, (j+1)H) of Wqkv
-      ok &= up_bf16(L.wqkv + static_cast<size_t>(j) * H * H, take(static_cast<size_t>(H) * H),
-                    static_cast<size_t>(H) * H) == cudaSuccess;
+      // (E4M3 rows are H bytes: matrix j starts at byte j H H, i.e. element j H H / 2)
+      ok &= up_mat(L.wqkv + static_cast<size_t>(j) * H * H / (f8 ? 2 : 1), take(static_cast<size_t>(H) * H), H, H,
+                   f8 ? L.sqkv + j * H : nullptr, 1.f / kF8ScaleHidden) == cudaSuccess;
       ok &= up_f32(L.bqkv + j * H, take(H), H) == cudaSuccess;
     }
-    ok &= up_bf16(L.wo, take(static_cast<size_t>(H) * H), static_cast<size_t>(H) * H) == cudaSuccess;
+    ok &= up_mat(L.wo, take(static_cast<size_t>(H) * H), H, H, L.so, 1.f / kF8ScaleCtx) == cudaSuccess;
     ok &= up_f32(L.bo, take(H), H) == cudaSuccess;
     ok &= up_f32(L.ln1g, take(H), H) == cudaSuccess;
     ok &= up_f32(L.ln1b, take(H), H) == cudaSuccess;
-    ok &= up_bf16(L.w1, take(static_cast<size_t>(F) * H), static_cast<size_t>(F) * H) == cudaSuccess;
+    ok &= up_mat(L.w1, take(static_cast<size_t>(F) * H), F, H, L.s1, 1.f / kF8ScaleHidden) == cudaSuccess;
     ok &= up_f32(L.b1, take(F), F) == cudaSuccess;
-    ok &= up_bf16(L.w2, take(static_cast<size_t>(H) * F), static_cast<size_t>(H) * F) == cudaSuccess;
+    ok &= up_mat(L.w2, take(static_cast<size_t>(H) * F), H, F, L.s2, 1.f / kF8ScaleGelu) == cudaSuccess;
     ok &= up_f32(L.b2, take(H), H) == cudaSuccess;
     ok &= up_f32(L.ln2g, take(H), H) == cudaSuccess;
     ok &= up_f32(L.ln2b, take(H), H) == cudaSuccess;
@@ -401,10 +430,21 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   for (int l = 0; l < cfg->num_layers; ++l) {
     Layer& L = p->layers[l];
     // out-proj and FFN2 carry the residual add + LayerNorm in their epilogue (in place on h32)
-    bool ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
-              make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
-              make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
-              make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
+    bool ok;
+    if (f8)  // E4M3 operands in the same (bf16-sized) activation buffers
+      ok = make_gemm_plan_f8(&L.p_qkv, p->hb, T, L.wqkv, L.sqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16,
+                             1.f) &&
+           make_gemm_plan_f8(&L.p_out, p->ctx, T, L.wo, L.so, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN,
+                             kF8ScaleHidden) &&
+           make_gemm_plan_f8(&L.p_ffn1, p->hb, T, L.w1, L.s1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16,
+                             kF8ScaleGelu) &&
+           make_gemm_plan_f8(&L.p_ffn2, p->g, T, L.w2, L.s2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN,
+                             kF8ScaleHidden);
+    else
+      ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
+           make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
+           make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
+           make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
     // head dim 64: QKV written head-major ([3 nh][T][64]) for the tcgen05 attention's TMA boxes
     if (H / cfg->num_heads == 64) ok = ok && gemm_plan_set_head_major(&L.p_qkv, p->qkv, T);
     ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
@@ -438,14 +478,15 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
          launch_meta(lengths, n, total_tokens, c.max_position, p->cu, p->work, p->num_work, p->err, p->tile_q, st));
   LAUNCH(p, PC_EMBED, st,
          launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
-                         p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err, st));
+                         p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err,
+                         c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, st));
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     LAUNCH(p, PC_ATTN, st,
            launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
-                            st));
+                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, st));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
@@ -752,6 +793,46 @@ elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias
   return ELIS_OK;
 }
 
+elis_status elis_op_quant_rows_e4m3(const float* W, int32_t rows, int32_t cols, uint8_t* q, float* scale, float post,
+                                   void* stream) {
+  if (!W || !q || !scale || rows < 1 || cols < 4 || cols % 4) return fail(ELIS_ERR_INVALID_ARG, "quant arguments");
+  CUDA_TRY(launch_quant_rows_e4m3(W, rows, cols, q, scale, post, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_gemm_f8(const uint8_t* A, const uint8_t* W, const float* colscale, const float* bias, void* out,
+                            int32_t M, int32_t N, int32_t K, int32_t epilogue, float out_scale, void* stream) {
+  if (!A || !W || !colscale || !bias || !out || M < 1 || N < 256 || N % 256 || K < 128 || K % 128 ||
+      (epilogue != ELIS_EPI_BIAS_BF16 && epilogue != ELIS_EPI_BIAS_GELU_BF16))
+    return fail(ELIS_ERR_INVALID_ARG, "gemm_f8 arguments");
+  GemmPlan g;
+  if (!make_gemm_plan_f8(&g, A, M, W, colscale, bias, nullptr, out, M, N, K, epilogue, out_scale))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_gemm_ln_f8(const uint8_t* A, const uint8_t* W, const float* colscale, const float* bias,
+                               float* resid_inout, const float* gamma, const float* beta, float eps, uint8_t* outb,
+                               float out_scale, int32_t M, int32_t N, int32_t K, void* stream) {
+  if (!A || !W || !colscale || !bias || !resid_inout || !gamma || !beta || !outb || M < 1 || N < 256 || N % 256 ||
+      N / 256 > 4 || K < 128 || K % 128)
+    return fail(ELIS_ERR_INVALID_ARG, "gemm_ln_f8 arguments");
+  GemmPlan g;
+  if (!make_gemm_plan_f8(&g, A, M, W, colscale, bias, resid_inout, resid_inout, M, N, K, EPI_BIAS_RESID_LN,
+                         out_scale) ||
+      !gemm_plan_set_ln(&g, reinterpret_cast<uint16_t*>(outb), gamma, beta, eps, static_cast<uint64_t>(M)))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
 elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* bias, float* resid_inout,
                             const float* gamma, const float* beta, float eps, uint16_t* outb, int32_t M, int32_t N,
                             int32_t K, void* stream) {
@@ -790,7 +871,7 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(AttnWork)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);

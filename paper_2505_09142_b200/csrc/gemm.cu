@@ -87,8 +87,8 @@ struct SmemPlan {
   static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
   static constexpr int STG_WARP = NSTG * ((OUT_F32 ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
   static constexpr int STG_BYTES = kEpiWarps * STG_WARP;
-  // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta[256] f32
-  static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 3 * 256 * 4;
+  // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta/colscale[256] f32
+  static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 4 * 256 * 4;
   static constexpr int SMEM_BYTES = STAGES * GemmCfg<BN>::STAGE_BYTES + RES_BYTES + STG_BYTES + AUX_BYTES + 1024;
   static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
@@ -140,8 +140,23 @@ ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, floa
 ELIS_DEV uint32_t sw128_off(int r, int k) { return static_cast<uint32_t>(r * 128 + ((k ^ (r & 7)) << 4)); }
 // Same for 64-byte rows, SWIZZLE_64B (16-byte pieces XOR bits [7,9) of the offset).
 ELIS_DEV uint32_t sw64_off(int r, int k) { return static_cast<uint32_t>(r * 64 + ((k ^ ((r >> 1) & 3)) << 4)); }
+// Same for 32-byte rows, SWIZZLE_32B (16-byte pieces XOR bit 7 of the offset): the E4M3 boxes.
+ELIS_DEV uint32_t sw32_off(int r, int k) { return static_cast<uint32_t>(r * 32 + ((k ^ ((r >> 2) & 1)) << 4)); }
 
-template <int BN, int EPI, bool DEEP>
+// 32 values of one row -> E4M3(scale * v) into a 32-byte row of a SWIZZLE_32B staging box.
+ELIS_DEV void stage_e4m3_row(uint8_t* b, int lane, const float (&v)[32], float scale) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = pack_e4m3x4(v[16 * k + 4 * j] * scale, v[16 * k + 4 * j + 1] * scale, v[16 * k + 4 * j + 2] * scale,
+                         v[16 * k + 4 * j + 3] * scale);
+    *reinterpret_cast<uint4*>(b + sw32_off(lane, k)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+template <int BN, int EPI, bool DEEP, bool F8>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
@@ -152,6 +167,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr bool LN = SP::LN;
   constexpr bool RES = SP::RES;
   constexpr int STAGES = SP::STAGES;
+  // K elements per 128-byte operand row: 64 bf16 or 128 E4M3 (4 MMAs of K 16 / K 32 either way)
+  constexpr int BKE = F8 ? 2 * BK : BK;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -172,13 +189,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   float* sbias = reinterpret_cast<float*>(part + 2 * 128);   // [256]
   float* sgam = sbias + 256;                                 // [256]
   float* sbet = sgam + 256;                                  // [256]
+  float* sscale = sbet + 256;                                // [256] F8: per-column dequant scale
 
   const int warp = warp_id();
   const int lane = lane_id();
   const int M = args.M, N = args.N, K = args.K;
   const int num_m = (M + 2 * BM - 1) / (2 * BM);  // 256-row pair tiles
   const int num_n = N / BN;
-  const int num_k = K / BK;
+  const int num_k = K / BKE;
   // Cluster = (LN ? num_n : 1) pairs.  CTA rank r: pair r >> 1, half (row half / B half) r & 1.
   const int crank = static_cast<int>(cluster_ctarank());
   const int cpairs = LN ? num_n : 1;
@@ -228,8 +246,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           GT_ADD(0, GT_CLK() - g0);
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
           const uint32_t bar = mapa_shared(smem_u32(&full[s]), leader_rank);
-          tma_load_2d_pair(sA + s * C::A_BYTES, &tmA, bar, kb * BK, m * 2 * BM + hrow * BM);
-          tma_load_2d_pair(sB + s * C::B_BYTES, &tmB, bar, kb * BK, n * BN + hrow * C::B_ROWS);
+          tma_load_2d_pair(sA + s * C::A_BYTES, &tmA, bar, kb * BKE, m * 2 * BM + hrow * BM);
+          tma_load_2d_pair(sB + s * C::B_BYTES, &tmB, bar, kb * BKE, n * BN + hrow * C::B_ROWS);
           if (++s == STAGES) { s = 0; ph ^= 1u; }
         }
       }
@@ -237,7 +255,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA, one thread) for the pair
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16_f32(2 * BM, BN);
+      constexpr uint32_t idesc = F8 ? make_idesc_e4m3_f32(2 * BM, BN) : make_idesc_bf16_f32(2 * BM, BN);
       const uint16_t mask = static_cast<uint16_t>(3u << leader_rank);
       int s = 0;
       uint32_t ph = 0;
@@ -259,9 +277,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint64_t da = make_sw128_desc(smem_u32(sA + s * C::A_BYTES));
           const uint64_t db = make_sw128_desc(smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle row
-            tc_mma_f16_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {
+            // advance 32 bytes (16 bf16 / 32 E4M3) along K inside the 128-byte swizzle row
+            if constexpr (F8) tc_mma_f8_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            else tc_mma_f16_pair(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit_pair_mc(&empty[s], mask);
           if (++s == STAGES) { s = 0; ph ^= 1u; }
@@ -288,6 +307,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     auto stage_vectors = [&](int n) {    // bias (+ gamma, beta) of tile columns -> shared memory
       if (etid < BN) {
         sbias[etid] = __ldg(args.bias + n * BN + etid);
+        if constexpr (F8) sscale[etid] = __ldg(args.colscale + n * BN + etid);
         if constexpr (LN) {
           sgam[etid] = __ldg(args.gamma + n * BN + etid);
           sbet[etid] = __ldg(args.beta + n * BN + etid);
@@ -367,10 +387,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const float4 bb = *reinterpret_cast<const float4*>(sbias + tcol + j);
-          v[j + 0] = __uint_as_float(r[c & 1][j + 0]) + bb.x;
-          v[j + 1] = __uint_as_float(r[c & 1][j + 1]) + bb.y;
-          v[j + 2] = __uint_as_float(r[c & 1][j + 2]) + bb.z;
-          v[j + 3] = __uint_as_float(r[c & 1][j + 3]) + bb.w;
+          if constexpr (F8) {
+            const float4 sc = *reinterpret_cast<const float4*>(sscale + tcol + j);
+            v[j + 0] = fmaf(__uint_as_float(r[c & 1][j + 0]), sc.x, bb.x);
+            v[j + 1] = fmaf(__uint_as_float(r[c & 1][j + 1]), sc.y, bb.y);
+            v[j + 2] = fmaf(__uint_as_float(r[c & 1][j + 2]), sc.z, bb.z);
+            v[j + 3] = fmaf(__uint_as_float(r[c & 1][j + 3]), sc.w, bb.w);
+          } else {
+            v[j + 0] = __uint_as_float(r[c & 1][j + 0]) + bb.x;
+            v[j + 1] = __uint_as_float(r[c & 1][j + 1]) + bb.y;
+            v[j + 2] = __uint_as_float(r[c & 1][j + 2]) + bb.z;
+            v[j + 3] = __uint_as_float(r[c & 1][j + 3]) + bb.w;
+          }
         }
         if constexpr (RES) {
           const int s = c % NRES;
@@ -412,11 +440,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
             }
+            if constexpr (F8 && EPI == EPI_BIAS_GELU_BF16) {
+              stage_e4m3_row(b, lane, v, args.out_scale);
+            } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              *reinterpret_cast<uint4*>(b + sw64_off(lane, k)) =
-                  make_uint4(pack_bf16x2(v[8 * k + 0], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
-                             pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+              for (int k = 0; k < 4; ++k)
+                *reinterpret_cast<uint4*>(b + sw64_off(lane, k)) =
+                    make_uint4(pack_bf16x2(v[8 * k + 0], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
+                               pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+            }
           }
           issue_store(b, row0, col0);
         }
@@ -486,11 +518,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             *reinterpret_cast<float4*>(b + sw128_off(lane, k)) =
                 make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
           uint8_t* bb = b + SP::STG_F32;
+          if constexpr (F8) {
+            stage_e4m3_row(bb, lane, y, args.out_scale);
+          } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<uint4*>(bb + sw64_off(lane, k)) =
-                make_uint4(pack_bf16x2(y[8 * k + 0], y[8 * k + 1]), pack_bf16x2(y[8 * k + 2], y[8 * k + 3]),
-                           pack_bf16x2(y[8 * k + 4], y[8 * k + 5]), pack_bf16x2(y[8 * k + 6], y[8 * k + 7]));
+            for (int k = 0; k < 4; ++k)
+              *reinterpret_cast<uint4*>(bb + sw64_off(lane, k)) =
+                  make_uint4(pack_bf16x2(y[8 * k + 0], y[8 * k + 1]), pack_bf16x2(y[8 * k + 2], y[8 * k + 3]),
+                             pack_bf16x2(y[8 * k + 4], y[8 * k + 5]), pack_bf16x2(y[8 * k + 6], y[8 * k + 7]));
+          }
           issue_store(b, row0, col0);
         }
         if (gt_me) GT_ADD(7, GT_CLK() - g1);
@@ -518,10 +554,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int BN, int EPI, bool DEEP>
+template <int BN, int EPI, bool DEEP, bool F8 = false>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   using SP = SmemPlan<BN, EPI, DEEP>;
-  auto kern = k_gemm_tc<BN, EPI, DEEP>;
+  auto kern = k_gemm_tc<BN, EPI, DEEP, F8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
@@ -546,7 +582,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   // number of clusters that can be co-resident (one CTA per SM)
-  static int max_clusters[2 * kMaxCluster + 1] = {};  // per (BN, EPI, DEEP) instantiation
+  static int max_clusters[2 * kMaxCluster + 1] = {};  // per (BN, EPI, DEEP, F8) instantiation
   if (max_clusters[csize] == 0) {
     cudaLaunchConfig_t q = cfg;
     q.gridDim = dim3(csize * (num_sms / csize));
@@ -570,6 +606,17 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
   if (g.args.M <= 0) return cudaSuccess;
   const bool b256 = gemm_block_n(g.args.N) == 256;
   const bool deep = g.args.K >= 2048;  // long mainloop: a 4th operand stage beats a 2nd residual slot
+  if (g.f8) {  // E4M3 operands: the BGE-base / large shapes (every N a multiple of 256)
+    if (!b256) return cudaErrorInvalidValue;
+    switch (g.epi) {
+      case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, true>(g, num_sms, st);
+      case EPI_BIAS_GELU_BF16: return launch_bn<256, EPI_BIAS_GELU_BF16, false, true>(g, num_sms, st);
+      case EPI_BIAS_RESID_LN:
+        return deep ? launch_bn<256, EPI_BIAS_RESID_LN, true, true>(g, num_sms, st)
+                    : launch_bn<256, EPI_BIAS_RESID_LN, false, true>(g, num_sms, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (g.epi) {
     case EPI_BIAS_BF16:
       return b256 ? launch_bn<256, EPI_BIAS_BF16, false>(g, num_sms, st)
@@ -636,6 +683,7 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
   if (N % 128 != 0 || K % BK != 0 || M < 0) return false;
   if (epi == EPI_BIAS_RESID_LN && N / gemm_block_n(N) > kMaxCluster) return false;
   g->epi = epi;
+  g->f8 = 0;
   g->args = GemmArgs{};
   g->args.M = M;
   g->args.N = N;
@@ -658,6 +706,29 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
   } else {
     if (!make_tmap_2d(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, a_rows, N, kBox, kBox,
                       CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
+    g->tmR = g->tmO;
+    g->tmOb = g->tmO;
+  }
+  return true;
+}
+
+bool make_gemm_plan_f8(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* colscale,
+                       const float* bias, const float* resid, void* out, int M, int N, int K, int epi,
+                       float out_scale) {
+  if (N % 256 != 0 || K % (2 * BK) != 0 || M < 0 || !colscale || epi == EPI_BIAS_RESID_F32) return false;
+  if (!make_gemm_plan(g, A, a_rows, W, bias, resid, out, M, N, K, epi)) return false;
+  g->f8 = 1;
+  g->args.colscale = colscale;
+  g->args.out_scale = out_scale;
+  // operands: 128 E4M3 (= 128 bytes, one SWIZZLE_128B row) x rows boxes
+  if (!make_tmap_2d(&g->tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, A, a_rows, K, 2 * BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_tmap_2d(&g->tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, W, N, K, 2 * BK, gemm_block_n(N) / 2,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  if (epi == EPI_BIAS_GELU_BF16) {  // E4M3 output, 32 x 32-byte boxes (SWIZZLE_32B)
+    if (!make_tmap_2d(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, out, a_rows, N, kBox, kBox,
+                      CU_TENSOR_MAP_SWIZZLE_32B))
       return false;
     g->tmR = g->tmO;
     g->tmOb = g->tmO;
@@ -688,6 +759,9 @@ bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const flo
   g->args.gamma = gamma;
   g->args.beta = beta;
   g->args.eps = eps;
+  if (g->f8)
+    return make_tmap_2d(&g->tmOb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, outb, rows, g->args.N, kBox, kBox,
+                        CU_TENSOR_MAP_SWIZZLE_32B);
   return make_tmap_2d(&g->tmOb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, outb, rows, g->args.N, kBox, kBox,
                       CU_TENSOR_MAP_SWIZZLE_64B);
 }

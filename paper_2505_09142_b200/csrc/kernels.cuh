@@ -23,6 +23,11 @@ struct GemmArgs {
   float eps;
   int M, N, K;
   int out_head_major;   // bf16 output written as [N/64 planes][rows][64] (attention-friendly qkv)
+  // FP8 (E4M3) operands (R20): acc * colscale[n] = A W^T in real units (the weight's
+  // per-output-channel scale over the A operand's static power-of-two scale); the GELU output
+  // and the LN epilogue's normalised copy are written as E4M3(out_scale * value)
+  const float* colscale;
+  float out_scale;
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major
@@ -32,12 +37,18 @@ struct GemmPlan {
   CUtensorMap tmOb;  // RESID_LN: bf16 copy of the normalised rows, 32 x 32 boxes
   GemmArgs args;
   int epi;
+  int f8;            // operands E4M3 (kind::f8f6f4): A [M, K] / W [N, K] bytes, 128-element K blocks
 };
 // bf16 output in head-major planes: out[N/64][rows][64] (the QKV projection feeding attention:
 // every (head, 128-token) box of Q, K or V is one contiguous 16 KB block)
 bool gemm_plan_set_head_major(GemmPlan* g, void* out, uint64_t rows);
-// LN epilogue outputs: outb bf16 [rows, N], gamma/beta f32 [N]
+// LN epilogue outputs: outb bf16 [rows, N] (E4M3 bytes when g->f8), gamma/beta f32 [N]
 bool gemm_plan_set_ln(GemmPlan* g, uint16_t* outb, const float* gamma, const float* beta, float eps, uint64_t rows);
+// FP8 variant of make_gemm_plan: A E4M3 [a_rows, K], W E4M3 [N, K], colscale f32 [N]; the
+// EPI_BIAS_GELU_BF16 output (and the LN copy) become E4M3 bytes scaled by out_scale
+bool make_gemm_plan_f8(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* colscale,
+                       const float* bias, const float* resid, void* out, int M, int N, int K, int epi,
+                       float out_scale);
 int gemm_block_n(int N);
 bool make_tmap_bf16_kmajor(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 // bf16 [rows, cols] row-major, box {box_cols (<= 64 for SWIZZLE_128B), box_rows}, SWIZZLE_128B
@@ -64,7 +75,11 @@ cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_po
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
                             int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
                             const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
-                            uint16_t* hb, uint32_t* err, cudaStream_t st);
+                            uint16_t* hb, uint32_t* err, float f8_scale, cudaStream_t st);
+// f8_scale > 0: hb receives E4M3(f8_scale * LN(x)) bytes [T, H] instead of bf16
+// FP8 weights: q [rows, cols] = E4M3(W * 448 / amax_row), scale[row] = amax_row / 448 * post
+cudaError_t launch_quant_rows_e4m3(const float* W, int rows, int cols, uint8_t* q, float* scale, float post,
+                                   cudaStream_t st);
 cudaError_t launch_layernorm(const float* u, const float* gamma, const float* beta, float eps, int64_t rows, int H,
                              float* out32, uint16_t* outb, cudaStream_t st);
 
@@ -78,10 +93,11 @@ inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_ma
 // head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
 // grid: one CTA per (work item, head), head fastest, so the list's cost order is the launch order
-// head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H]
+// head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H].
+// ctx_f8_scale > 0 (head dim 64 only): ctx is written as E4M3(ctx_f8_scale * ctx) bytes [T, H]
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, cudaStream_t st);
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,

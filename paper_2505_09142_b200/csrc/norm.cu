@@ -110,7 +110,8 @@ struct RowLayout {
 
 template <int H>
 __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamma, const float* __restrict__ beta,
-                              float eps, float* __restrict__ out32, uint16_t* __restrict__ outb, int lane) {
+                              float eps, float* __restrict__ out32, uint16_t* __restrict__ outb, int lane,
+                              float f8_scale = 0.f) {
   using RL = RowLayout<H>;
   float s = 0.f;
 #pragma unroll
@@ -134,7 +135,11 @@ __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamm
       float4* o = reinterpret_cast<float4*>(out32 + base);
       o[0] = make_float4(y[0], y[1], y[2], y[3]);
       o[1] = make_float4(y[4], y[5], y[6], y[7]);
-      if (outb)
+      if (outb && f8_scale > 0.f)  // E4M3 bytes (FP8 GEMM operand, R20)
+        *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(outb) + base) =
+            make_uint2(pack_e4m3x4(y[0] * f8_scale, y[1] * f8_scale, y[2] * f8_scale, y[3] * f8_scale),
+                       pack_e4m3x4(y[4] * f8_scale, y[5] * f8_scale, y[6] * f8_scale, y[7] * f8_scale));
+      else if (outb)
         *reinterpret_cast<uint4*>(outb + base) =
             make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
     } else {
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
                                                   const uint16_t* __restrict__ word, const uint16_t* __restrict__ pos,
                                                   const uint16_t* __restrict__ type0, const float* __restrict__ gamma,
                                                   const float* __restrict__ beta, float eps, float* __restrict__ h32,
-                                                  uint16_t* __restrict__ hb, uint32_t* __restrict__ err) {
+                                                  uint16_t* __restrict__ hb, uint32_t* __restrict__ err, float f8_scale) {
   using RL = RowLayout<H>;
   const int lane = lane_id();
   const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp_id();
@@ -201,8 +206,10 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
 #pragma unroll
     for (int k = 0; k < RL::C; ++k) x[j * RL::C + k] = a[k] + b[k] + c[k];
   }
-  ln_finish_row<H>(x, gamma, beta, eps, h32 + static_cast<size_t>(t) * H, hb ? hb + static_cast<size_t>(t) * H : nullptr,
-                   lane);
+  uint16_t* hrow = nullptr;
+  if (hb) hrow = f8_scale > 0.f ? reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(hb) + static_cast<size_t>(t) * H)
+                                : hb + static_cast<size_t>(t) * H;
+  ln_finish_row<H>(x, gamma, beta, eps, h32 + static_cast<size_t>(t) * H, hrow, lane, f8_scale);
 }
 
 template <int H>
@@ -232,7 +239,36 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ u, 
                    outb ? outb + static_cast<size_t>(r) * H : nullptr, lane);
 }
 
+// FP8 weight preparation (create time, R20): row r of W f32 [rows, cols] ->
+// q[r, :] = E4M3(W[r, :] * 448 / amax_r) and scale[r] = amax_r / 448 * post (the GEMM epilogue's
+// per-output-channel dequantisation, with the A operand's static scale folded in as `post`).
+__global__ void __launch_bounds__(256) k_quant_rows_e4m3(const float* __restrict__ W, int cols, uint8_t* __restrict__ q,
+                                                         float* __restrict__ scale, float post) {
+  __shared__ float red[8];
+  const float* src = W + static_cast<size_t>(blockIdx.x) * cols;
+  float a = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) a = fmaxf(a, fabsf(src[c]));
+  a = warp_max(a);
+  if (lane_id() == 0) red[warp_id()] = a;
+  __syncthreads();
+  float amax = 0.f;
+  for (int w = 0; w < 8; ++w) amax = fmaxf(amax, red[w]);
+  const float inv = amax > 0.f ? 448.f / amax : 1.f;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(q + static_cast<size_t>(blockIdx.x) * cols);
+  for (int c = threadIdx.x; c < cols / 4; c += blockDim.x)
+    dst[c] = pack_e4m3x4(src[4 * c] * inv, src[4 * c + 1] * inv, src[4 * c + 2] * inv, src[4 * c + 3] * inv);
+  if (threadIdx.x == 0) scale[blockIdx.x] = (amax > 0.f ? amax / 448.f : 1.f) * post;
+}
+
 }  // namespace
+
+cudaError_t launch_quant_rows_e4m3(const float* W, int rows, int cols, uint8_t* q, float* scale, float post,
+                                   cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  if (cols % 4 != 0) return cudaErrorInvalidValue;
+  k_quant_rows_e4m3<<<rows, 256, 0, st>>>(W, cols, q, scale, post);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
                         AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st) {
@@ -251,11 +287,11 @@ cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_po
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H, int vocab,
                             int max_position, const uint16_t* word, const uint16_t* pos, const uint16_t* type0,
                             const float* gamma, const float* beta, float eps, float* h32, uint16_t* hb, uint32_t* err,
-                            cudaStream_t st) {
+                            float f8_scale, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
   ELIS_H_DISPATCH(H, (k_embed_ln<HH><<<grid, 256, 0, st>>>(tokens, cu_seqlens, n, T, vocab, max_position, word, pos,
-                                                            type0, gamma, beta, eps, h32, hb, err)));
+                                                            type0, gamma, beta, eps, h32, hb, err, f8_scale)));
   return cudaGetLastError();
 }
 

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--lengths", default="trace")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print per-kernel ms from the library profiler")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"])
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
     if a.lengths == "trace":
@@ -36,7 +37,8 @@ def main():
         L = np.full(a.n, int(a.lengths.split(":")[1]), np.int32)
     tok = inputs.make_tokens(L, seed=0)
     T = int(L.sum())
-    p = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg)), max_tokens=T, max_requests=a.n)
+    p = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg)), max_tokens=T, max_requests=a.n,
+                         precision=a.precision)
     dev = torch.device("cuda:0")
     t_tok = torch.from_numpy(tok).to(dev)
     t_len = torch.from_numpy(L.astype(np.int32)).to(dev)

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert binding.lib().elis_abi_version() == 2
+    assert binding.lib().elis_abi_version() == binding.ABI_VERSION == 3
 
 
 @pytest.mark.parametrize("name", ["tiny", "base", "large"])
@@ -85,3 +85,15 @@ def test_null_argument_errors_without_gpu():
     assert L.elis_predict_remaining(None, None, None, 1, 1, None, None, None) == 1
     assert L.elis_isrtf_select(None, None, None, 1, 1, None, None, None) == 1
     assert L.elis_sync_status(None) == 1
+
+
+def test_precision_validation():
+    """FP8 needs head dim 64 and 256-multiples; unknown precisions fail."""
+    L = binding.lib()
+    ok = binding.make_config(inputs.CONFIGS["base"], 1024, 16, precision="fp8")
+    assert L.elis_weight_count(ctypes.byref(ok)) == inputs.weight_count(inputs.CONFIGS["base"])
+    tiny = binding.make_config(inputs.CONFIGS["tiny"], 1024, 16, precision="fp8")
+    assert L.elis_weight_count(ctypes.byref(tiny)) == 0
+    bad = binding.make_config(inputs.CONFIGS["base"], 1024, 16)
+    bad.precision = 7
+    assert L.elis_weight_count(ctypes.byref(bad)) == 0
