@@ -48,9 +48,11 @@ def parse():
     ap.add_argument("--lengths", default="trace", help="trace | uniform | fixed:L")
     ap.add_argument("--cap", type=int, default=4, help="batch_cap")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--precision", choices=["bf16", "fp8"], default="bf16",
-                    help="encoder GEMM operands: bf16 (default, the parity-bound path) or fp8 E4M3 "
-                         "(SURVEY.md 8f row f4(i); looser tolerance, DESIGN.md R20)")
+    ap.add_argument("--precision", choices=["bf16", "fp8", "fp16"], default=None,
+                    help="encoder operands: fp16 (default where supported: head dim 64; SURVEY.md 8f row "
+                         "f4(iii) -- the precision that meets the north_star parity bars on every tested "
+                         "input at bf16's speed, DESIGN.md R21), bf16 (default for the tiny d=32 encoder), or "
+                         "fp8 E4M3 GEMMs (row f4(i); looser tolerance, DESIGN.md R20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=12, help="requests in the oracle sample")
     ap.add_argument("--inflight", type=int, default=0,
@@ -443,14 +445,15 @@ def run_elis(args):
     out = None
     if rank == 0:
         peaks = load_peaks()
-        roof = kernel_roofline(prof, cfg, T_roof, L, peaks, load_traffic() if args.precision == "bf16" else {},
+        roof = kernel_roofline(prof, cfg, T_roof, L, peaks, load_traffic() if args.precision in ("bf16", "fp16") else {},
                                fp8=args.precision == "fp8")
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "ms_per_step_p10_p50_p90": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90)],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16" if args.precision == "bf16" else "fp8_e4m3 GEMMs (bf16 attention, fp32 residual/LN/head)",
+            "dtype": {"bf16": "bf16", "fp16": "fp16",
+                      "fp8": "fp8_e4m3 GEMMs (bf16 attention, fp32 residual/LN/head)"}[args.precision],
             "data": "synthetic (seeded trace-shaped lengths, uniform token ids, random-init BGE weights)",
             "config": config_desc(args, T_roof, world),
             "tokens_per_s": round(world * T * args.steps / (total_ms / 1e3), 1),
@@ -478,6 +481,8 @@ def run_elis(args):
 
 def main():
     args = parse()
+    if args.precision is None:
+        args.precision = "fp16" if inputs.CONFIGS[args.config].head_dim == 64 else "bf16"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -60,8 +60,11 @@ typedef enum { ELIS_POLICY_ISRTF = 0, ELIS_POLICY_FCFS = 1 } elis_policy; /* P:2
  * FP8:  E4M3 weights (per-output-channel scale) and E4M3 activations (static power-of-two
  *       scales) on tcgen05 kind::f8f6f4, fp32 accumulate; attention stays bf16, the residual
  *       stream / LayerNorm / head stay fp32 (R20).
- *       Requires head dim 64 and hidden, intermediate multiples of 256 (BGE-base / large). */
-typedef enum { ELIS_PREC_BF16 = 0, ELIS_PREC_FP8 = 1 } elis_precision;
+ *       Requires head dim 64 and hidden, intermediate multiples of 256 (BGE-base / large).
+ * FP16: fp16 weights, GEMM/attention operands (Q, K, V, P) and 16-bit activations, fp32
+ *       accumulate; 3 more mantissa bits than bf16, same speed.
+ *       Same shape requirements as FP8. */
+typedef enum { ELIS_PREC_BF16 = 0, ELIS_PREC_FP8 = 1, ELIS_PREC_FP16 = 2 } elis_precision;
 
 /* Encoder + head shape.  BGE-base = {30522, 512, 2, 12, 768, 12, 3072}
  * (P:121, P:123 [Sec. 3.1]); head = 8 layers, hidden 1024. */

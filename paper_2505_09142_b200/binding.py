@@ -24,7 +24,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 
           6: "nccl", 7: "device input"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
 EPI_BIAS_BF16, EPI_BIAS_GELU_BF16, EPI_BIAS_RESID_F32 = 0, 1, 2
-PRECISION = {"bf16": 0, "fp8": 1}  # elis_precision
+PRECISION = {"bf16": 0, "fp8": 1, "fp16": 2}  # elis_precision
 
 _vp, _i32, _i64, _u32, _f32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
                                     ctypes.c_float, ctypes.c_size_t)

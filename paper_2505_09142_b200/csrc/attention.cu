@@ -308,7 +308,8 @@ ELIS_DEV constexpr bool exp2_on_fma(int pair) {
 }
 
 // F8OUT: ctx written as E4M3(ctx_scale * ctx) bytes [T, H] (the FP8 out-projection's A operand)
-template <bool F8OUT>
+// F16: Q, K, V, P and ctx in fp16 instead of bf16 (fp16 operand precision)
+template <bool F8OUT, bool F16>
 __global__ void __launch_bounds__(128, 4)
     k_attention_tc(const __grid_constant__ CUtensorMap tm,
                    const AttnWork* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
@@ -368,8 +369,8 @@ __global__ void __launch_bounds__(128, 4)
   // MMA rows are independent)
   const bool warp_active = q0 + warp * 32 < L;
 
-  constexpr uint32_t idesc_s = make_idesc_bf16_f32(TQ, TKB);
-  constexpr uint32_t idesc_o = make_idesc_bf16_f32(TQ, TD) | (1u << 16);  // B (V) is MN-major
+  constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB) : make_idesc_bf16_f32(TQ, TKB);
+  constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);  // V MN-major
   if (issuer) mbar_wait(q_full, 0);
   float m = -INFINITY, l = 0.f;   // running row max (scaled, log2 domain) and row sum
   unsigned long long o2[TD / 2];  // O as fp32 pairs
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(128, 4)
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
+        for (int e = 0; e < 16; ++e) pk[e] = pack16x2<F16>(p[2 * e], p[2 * e + 1]);
         tmem_st_32x32b_x16(taddr + c * 16, pk);
       }
     }
@@ -527,10 +528,10 @@ __global__ void __launch_bounds__(128, 4)
       uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        srow[k ^ (row & 7)] = make_uint4(pack_bf16x2(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
-                                         pack_bf16x2(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
-                                         pack_bf16x2(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
-                                         pack_bf16x2(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
+        srow[k ^ (row & 7)] = make_uint4(pack16x2<F16>(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
+                                         pack16x2<F16>(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
+                                         pack16x2<F16>(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
+                                         pack16x2<F16>(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
     }
   }
   tc_fence_before();
@@ -573,7 +574,7 @@ bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, cudaStream_t st) {
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
@@ -581,13 +582,15 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
   const unsigned grid = static_cast<unsigned>(max_tiles * num_heads);
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
-    auto kern = ctx_f8_scale > 0.f ? k_attention_tc<true> : k_attention_tc<false>;
+    if (f16 && ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
+    auto kern = f16 ? k_attention_tc<false, true> : ctx_f8_scale > 0.f ? k_attention_tc<true, false>
+                                                                       : k_attention_tc<false, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
     if (e != cudaSuccess) return e;
     kern<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
                                          static_cast<int>(plane_rows), ctx_f8_scale);
   } else if (d == 32) {
-    if (ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
+    if (ctx_f8_scale > 0.f || f16) return cudaErrorInvalidValue;
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, num_heads, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;

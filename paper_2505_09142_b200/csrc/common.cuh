@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -329,6 +330,21 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(uint32_t M, uint32_t 
          | (1u << 10)           // B format bf16
          | ((N >> 3) << 17)     // N >> 3
          | ((M >> 4) << 24);    // M >> 4
+}
+
+// Instruction descriptor, kind::f16 with fp16 A/B (format 0): D f32, both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t make_idesc_f16_f32(uint32_t M, uint32_t N) {
+  return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+ELIS_DEV uint32_t pack_half2(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);  // .x = lo (low 16 bits)
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// the 16-bit operand format of the active precision: fp16 when F16, else bf16
+template <bool F16>
+ELIS_DEV uint32_t pack16x2(float lo, float hi) {
+  if constexpr (F16) return pack_half2(lo, hi);
+  else return pack_bf16x2(lo, hi);
 }
 
 // Instruction descriptor, kind::f8f6f4: D f32, A/B E4M3 (format 0), both K-major, shape M x N.

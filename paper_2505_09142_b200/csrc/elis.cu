@@ -92,9 +92,10 @@ bool config_valid(const elis_config* c, std::string* why) {
   if (c->pooling != ELIS_POOL_MEAN && c->pooling != ELIS_POOL_CLS) return bad("pooling");
   if (c->head_layers < 2 || c->head_hidden < 1) return bad("head_layers >= 2, head_hidden >= 1");
   if (c->max_tokens < 1 || c->max_requests < 1) return bad("max_tokens / max_requests must be >= 1");
-  if (c->precision != ELIS_PREC_BF16 && c->precision != ELIS_PREC_FP8) return bad("precision");
-  if (c->precision == ELIS_PREC_FP8 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
-    return bad("FP8 needs head dim 64 and hidden, intermediate multiples of 256");
+  if (c->precision != ELIS_PREC_BF16 && c->precision != ELIS_PREC_FP8 && c->precision != ELIS_PREC_FP16)
+    return bad("precision");
+  if (c->precision != ELIS_PREC_BF16 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
+    return bad("FP8 / FP16 need head dim 64 and hidden, intermediate multiples of 256");
   return true;
 }
 
@@ -316,10 +317,17 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     return cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice);
   };
   const bool f8 = cfg->precision == ELIS_PREC_FP8;
+  const bool f16 = cfg->precision == ELIS_PREC_FP16;
+  auto up_f16 = [&](uint16_t* dst, const float* src, size_t n) {
+    std::vector<__half> tmp(n);
+    for (size_t i = 0; i < n; ++i) tmp[i] = __float2half_rn(src[i]);
+    return cudaMemcpy(dst, tmp.data(), n * 2, cudaMemcpyHostToDevice);
+  };
   float* wtmp = nullptr;  // FP8: fp32 staging of one matrix for the on-device quantiser
   if (f8 && p->alloc(&wtmp, static_cast<size_t>(F) * H) != cudaSuccess) return cleanup_fail(ELIS_ERR_OOM, "cudaMalloc wtmp");
   // encoder matrix [rows, cols] -> bf16, or E4M3 + per-row scale (x post) in FP8 mode
   auto up_mat = [&](uint16_t* dst, const float* src, int rows, int cols, float* sdst, float post) {
+    if (f16) return up_f16(dst, src, static_cast<size_t>(rows) * cols);
     if (!f8) return up_bf16(dst, src, static_cast<size_t>(rows) * cols);
     cudaError_t e = up_f32(wtmp, src, static_cast<size_t>(rows) * cols);
     if (e != cudaSuccess) return e;
@@ -445,6 +453,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
            make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
            make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
            make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN);
+    if (f16)  // fp16 operands: same 2-byte TMA boxes, fp16 instruction format and outputs
+      L.p_qkv.f16 = L.p_out.f16 = L.p_ffn1.f16 = L.p_ffn2.f16 = 1;
     // head dim 64: QKV written head-major ([3 nh][T][64]) for the tcgen05 attention's TMA boxes
     if (H / cfg->num_heads == 64) ok = ok && gemm_plan_set_head_major(&L.p_qkv, p->qkv, T);
     ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
@@ -479,14 +489,14 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   LAUNCH(p, PC_EMBED, st,
          launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
                          p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err,
-                         c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, st));
+                         c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, c.precision == ELIS_PREC_FP16, st));
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     LAUNCH(p, PC_ATTN, st,
            launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
-                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, st));
+                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, st));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
@@ -871,7 +881,7 @@ elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(AttnWork)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, false, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);

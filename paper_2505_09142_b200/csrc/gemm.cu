@@ -156,7 +156,8 @@ ELIS_DEV void stage_e4m3_row(uint8_t* b, int lane, const float (&v)[32], float s
   }
 }
 
-template <int BN, int EPI, bool DEEP, bool F8>
+// PREC: 0 bf16 operands, 1 E4M3 operands (kind::f8f6f4), 2 fp16 operands (16-bit outputs in fp16)
+template <int BN, int EPI, bool DEEP, int PREC>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
@@ -167,6 +168,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr bool LN = SP::LN;
   constexpr bool RES = SP::RES;
   constexpr int STAGES = SP::STAGES;
+  constexpr bool F8 = PREC == 1;
+  constexpr bool F16 = PREC == 2;
   // K elements per 128-byte operand row: 64 bf16 or 128 E4M3 (4 MMAs of K 16 / K 32 either way)
   constexpr int BKE = F8 ? 2 * BK : BK;
   extern __shared__ uint8_t smem_raw[];
@@ -255,7 +258,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA, one thread) for the pair
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = F8 ? make_idesc_e4m3_f32(2 * BM, BN) : make_idesc_bf16_f32(2 * BM, BN);
+      constexpr uint32_t idesc = F8    ? make_idesc_e4m3_f32(2 * BM, BN)
+                                 : F16 ? make_idesc_f16_f32(2 * BM, BN)
+                                       : make_idesc_bf16_f32(2 * BM, BN);
       const uint16_t mask = static_cast<uint16_t>(3u << leader_rank);
       int s = 0;
       uint32_t ph = 0;
@@ -446,8 +451,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 *reinterpret_cast<uint4*>(b + sw64_off(lane, k)) =
-                    make_uint4(pack_bf16x2(v[8 * k + 0], v[8 * k + 1]), pack_bf16x2(v[8 * k + 2], v[8 * k + 3]),
-                               pack_bf16x2(v[8 * k + 4], v[8 * k + 5]), pack_bf16x2(v[8 * k + 6], v[8 * k + 7]));
+                    make_uint4(pack16x2<F16>(v[8 * k + 0], v[8 * k + 1]), pack16x2<F16>(v[8 * k + 2], v[8 * k + 3]),
+                               pack16x2<F16>(v[8 * k + 4], v[8 * k + 5]), pack16x2<F16>(v[8 * k + 6], v[8 * k + 7]));
             }
           }
           issue_store(b, row0, col0);
@@ -524,8 +529,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               *reinterpret_cast<uint4*>(bb + sw64_off(lane, k)) =
-                  make_uint4(pack_bf16x2(y[8 * k + 0], y[8 * k + 1]), pack_bf16x2(y[8 * k + 2], y[8 * k + 3]),
-                             pack_bf16x2(y[8 * k + 4], y[8 * k + 5]), pack_bf16x2(y[8 * k + 6], y[8 * k + 7]));
+                  make_uint4(pack16x2<F16>(y[8 * k + 0], y[8 * k + 1]), pack16x2<F16>(y[8 * k + 2], y[8 * k + 3]),
+                             pack16x2<F16>(y[8 * k + 4], y[8 * k + 5]), pack16x2<F16>(y[8 * k + 6], y[8 * k + 7]));
           }
           issue_store(b, row0, col0);
         }
@@ -554,10 +559,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-template <int BN, int EPI, bool DEEP, bool F8 = false>
+template <int BN, int EPI, bool DEEP, int PREC = 0>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   using SP = SmemPlan<BN, EPI, DEEP>;
-  auto kern = k_gemm_tc<BN, EPI, DEEP, F8>;
+  auto kern = k_gemm_tc<BN, EPI, DEEP, PREC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
@@ -609,11 +614,22 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
   if (g.f8) {  // E4M3 operands: the BGE-base / large shapes (every N a multiple of 256)
     if (!b256) return cudaErrorInvalidValue;
     switch (g.epi) {
-      case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, true>(g, num_sms, st);
-      case EPI_BIAS_GELU_BF16: return launch_bn<256, EPI_BIAS_GELU_BF16, false, true>(g, num_sms, st);
+      case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, 1>(g, num_sms, st);
+      case EPI_BIAS_GELU_BF16: return launch_bn<256, EPI_BIAS_GELU_BF16, false, 1>(g, num_sms, st);
       case EPI_BIAS_RESID_LN:
-        return deep ? launch_bn<256, EPI_BIAS_RESID_LN, true, true>(g, num_sms, st)
-                    : launch_bn<256, EPI_BIAS_RESID_LN, false, true>(g, num_sms, st);
+        return deep ? launch_bn<256, EPI_BIAS_RESID_LN, true, 1>(g, num_sms, st)
+                    : launch_bn<256, EPI_BIAS_RESID_LN, false, 1>(g, num_sms, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (g.f16) {  // fp16 operands and 16-bit outputs
+    if (!b256) return cudaErrorInvalidValue;
+    switch (g.epi) {
+      case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, 2>(g, num_sms, st);
+      case EPI_BIAS_GELU_BF16: return launch_bn<256, EPI_BIAS_GELU_BF16, false, 2>(g, num_sms, st);
+      case EPI_BIAS_RESID_LN:
+        return deep ? launch_bn<256, EPI_BIAS_RESID_LN, true, 2>(g, num_sms, st)
+                    : launch_bn<256, EPI_BIAS_RESID_LN, false, 2>(g, num_sms, st);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -684,6 +700,7 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
   if (epi == EPI_BIAS_RESID_LN && N / gemm_block_n(N) > kMaxCluster) return false;
   g->epi = epi;
   g->f8 = 0;
+  g->f16 = 0;
   g->args = GemmArgs{};
   g->args.M = M;
   g->args.N = N;

@@ -38,6 +38,7 @@ struct GemmPlan {
   GemmArgs args;
   int epi;
   int f8;            // operands E4M3 (kind::f8f6f4): A [M, K] / W [N, K] bytes, 128-element K blocks
+  int f16;           // operands fp16 (kind::f16, A/B format f16); 16-bit outputs written as fp16
 };
 // bf16 output in head-major planes: out[N/64][rows][64] (the QKV projection feeding attention:
 // every (head, 128-token) box of Q, K or V is one contiguous 16 KB block)
@@ -75,8 +76,8 @@ cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_po
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
                             int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
                             const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
-                            uint16_t* hb, uint32_t* err, float f8_scale, cudaStream_t st);
-// f8_scale > 0: hb receives E4M3(f8_scale * LN(x)) bytes [T, H] instead of bf16
+                            uint16_t* hb, uint32_t* err, float f8_scale, bool f16, cudaStream_t st);
+// f8_scale > 0: hb receives E4M3(f8_scale * LN(x)) bytes [T, H] instead of bf16; f16: fp16
 // FP8 weights: q [rows, cols] = E4M3(W * 448 / amax_row), scale[row] = amax_row / 448 * post
 cudaError_t launch_quant_rows_e4m3(const float* W, int rows, int cols, uint8_t* q, float* scale, float post,
                                    cudaStream_t st);
@@ -94,10 +95,11 @@ inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_ma
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
 // grid: one CTA per (work item, head), head fastest, so the list's cost order is the launch order
 // head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H].
-// ctx_f8_scale > 0 (head dim 64 only): ctx is written as E4M3(ctx_f8_scale * ctx) bytes [T, H]
+// ctx_f8_scale > 0 (head dim 64 only): ctx is written as E4M3(ctx_f8_scale * ctx) bytes [T, H];
+// f16 (head dim 64 only): qkv and ctx are fp16 instead of bf16
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, cudaStream_t st);
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,

@@ -111,7 +111,7 @@ struct RowLayout {
 template <int H>
 __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamma, const float* __restrict__ beta,
                               float eps, float* __restrict__ out32, uint16_t* __restrict__ outb, int lane,
-                              float f8_scale = 0.f) {
+                              float f8_scale = 0.f, bool f16 = false) {
   using RL = RowLayout<H>;
   float s = 0.f;
 #pragma unroll
@@ -139,6 +139,9 @@ __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamm
         *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(outb) + base) =
             make_uint2(pack_e4m3x4(y[0] * f8_scale, y[1] * f8_scale, y[2] * f8_scale, y[3] * f8_scale),
                        pack_e4m3x4(y[4] * f8_scale, y[5] * f8_scale, y[6] * f8_scale, y[7] * f8_scale));
+      else if (outb && f16)
+        *reinterpret_cast<uint4*>(outb + base) =
+            make_uint4(pack_half2(y[0], y[1]), pack_half2(y[2], y[3]), pack_half2(y[4], y[5]), pack_half2(y[6], y[7]));
       else if (outb)
         *reinterpret_cast<uint4*>(outb + base) =
             make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
@@ -177,7 +180,8 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
                                                   const uint16_t* __restrict__ word, const uint16_t* __restrict__ pos,
                                                   const uint16_t* __restrict__ type0, const float* __restrict__ gamma,
                                                   const float* __restrict__ beta, float eps, float* __restrict__ h32,
-                                                  uint16_t* __restrict__ hb, uint32_t* __restrict__ err, float f8_scale) {
+                                                  uint16_t* __restrict__ hb, uint32_t* __restrict__ err, float f8_scale,
+                                                  bool f16) {
   using RL = RowLayout<H>;
   const int lane = lane_id();
   const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp_id();
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
   uint16_t* hrow = nullptr;
   if (hb) hrow = f8_scale > 0.f ? reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(hb) + static_cast<size_t>(t) * H)
                                 : hb + static_cast<size_t>(t) * H;
-  ln_finish_row<H>(x, gamma, beta, eps, h32 + static_cast<size_t>(t) * H, hrow, lane, f8_scale);
+  ln_finish_row<H>(x, gamma, beta, eps, h32 + static_cast<size_t>(t) * H, hrow, lane, f8_scale, f16);
 }
 
 template <int H>
@@ -287,11 +291,11 @@ cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_po
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H, int vocab,
                             int max_position, const uint16_t* word, const uint16_t* pos, const uint16_t* type0,
                             const float* gamma, const float* beta, float eps, float* h32, uint16_t* hb, uint32_t* err,
-                            float f8_scale, cudaStream_t st) {
+                            float f8_scale, bool f16, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
   ELIS_H_DISPATCH(H, (k_embed_ln<HH><<<grid, 256, 0, st>>>(tokens, cu_seqlens, n, T, vocab, max_position, word, pos,
-                                                            type0, gamma, beta, eps, h32, hb, err, f8_scale)));
+                                                            type0, gamma, beta, eps, h32, hb, err, f8_scale, f16)));
   return cudaGetLastError();
 }
 

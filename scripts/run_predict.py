@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--lengths", default="trace")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print per-kernel ms from the library profiler")
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8", "fp16"])
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
     if a.lengths == "trace":

@@ -83,28 +83,30 @@ def test_cfg1_tiny_full_parity_and_select(cuda_lib, pooling):
     P.close()
 
 
-def test_base_ragged_parity(cuda_lib):
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+def test_base_ragged_parity(cuda_lib, precision):
     """BGE-base, ragged lengths spanning several GEMM/attention tiles and ragged tails."""
     from oracle import head as ohead
     lengths = np.array([1, 7, 32, 63, 64, 65, 127, 128, 129, 300, 511, 512], dtype=np.int32)
-    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths))
+    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths), precision=precision)
     tokens = inputs.make_tokens(lengths, seed=2)
     gpu, hid = run_predict(P, lengths, tokens, with_hidden=True)
     ref, hs = ohead.predict_with_hidden(tokens, lengths, W, cfg)
     hidden_err = np.abs(hid.astype(np.float64) - np.concatenate(hs)).max()
     r = rel_err(gpu, ref)
-    print(f"base ragged: hidden max abs err {hidden_err:.4g}, pred max rel err {r.max():.4g}")
+    print(f"base ragged {precision}: hidden max abs err {hidden_err:.4g}, pred max rel err {r.max():.4g}")
     assert hidden_err <= HIDDEN_ATOL
     assert r.max() <= PRED_RTOL
     P.close()
 
 
-def test_batch_invariance_bitwise(cuda_lib):
+@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp8"])
+def test_batch_invariance_bitwise(cuda_lib, precision):
     """pred_i is bitwise identical whether request i is encoded alone, in a batch, or in a
     different batch order (row-independent GEMMs, per-request attention/pool/head)."""
     lengths = np.array([40, 200, 64, 1, 511, 77, 129], dtype=np.int32)
     tokens = inputs.make_tokens(lengths, seed=3)
-    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths))
+    cfg, W, P = make_predictor("base", int(lengths.sum()), len(lengths), precision=precision)
     full, _ = run_predict(P, lengths, tokens)
     starts = inputs.offsets(lengths)
     for i in (0, 3, 4):
@@ -170,7 +172,8 @@ def test_iteration_host_matches_device_path(cuda_lib):
     P.close()
 
 
-def test_cfg2_full_size_sampled_parity(cuda_lib):
+@pytest.mark.parametrize("precision,k", [("bf16", 6), ("fp16", 16)])
+def test_cfg2_full_size_sampled_parity(cuda_lib, precision, k):
     """BASELINE.json configs[1] at full size in the bench's launch configuration
     (BGE-base, 256 trace-shaped requests): sampled predictions vs the oracle, and the
     ISRTF batch bit-exact on the GPU's predictions."""
@@ -179,13 +182,13 @@ def test_cfg2_full_size_sampled_parity(cuda_lib):
     n = 256
     L, gen, _ = inputs.trace_lengths(n, seed=0)
     tokens = inputs.make_tokens(L, seed=0)
-    cfg, W, P = make_predictor("base", int(L.sum()), n)
+    cfg, W, P = make_predictor("base", int(L.sum()), n, precision=precision)
     gpu, _ = run_predict(P, L, tokens)
     order = np.argsort(L)
-    sample = sorted(set(order[np.linspace(0, n - 1, 6).astype(int)].tolist()))  # stratified by length
+    sample = sorted(set(order[np.linspace(0, n - 1, k).astype(int)].tolist()))  # stratified by length
     ref = ohead.predict(tokens, L, W, cfg, requests=sample)
     r = rel_err(gpu[sample], ref)
-    print("cfg2 sampled rel err", r.max(), "lengths", L[sample])
+    print(f"cfg2 {precision} sampled rel err", r.max(), "lengths", L[sample])
     assert r.max() <= PRED_RTOL
     assert np.isfinite(gpu).all()
     for cap in (4, 256):
@@ -196,7 +199,8 @@ def test_cfg2_full_size_sampled_parity(cuda_lib):
     P.close()
 
 
-def test_cfg3_large_4096_ragged_sampled_parity(cuda_lib):
+@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+def test_cfg3_large_4096_ragged_sampled_parity(cuda_lib, precision):
     """BASELINE.json configs[2]: BGE-large re-predicting 4,096 ragged requests of 32-512
     tokens (uniform lengths, T ~ 1.1M) in one call; stratified sample vs the oracle, the
     whole batch finite, and the batch invariance of a sampled request."""
@@ -204,14 +208,14 @@ def test_cfg3_large_4096_ragged_sampled_parity(cuda_lib):
     n = 4096
     L = inputs.uniform_lengths(n, 32, 512, seed=0)
     tokens = inputs.make_tokens(L, seed=7)
-    cfg, W, P = make_predictor("large", int(L.sum()), n)
+    cfg, W, P = make_predictor("large", int(L.sum()), n, precision=precision)
     gpu, _ = run_predict(P, L, tokens)
     assert np.isfinite(gpu).all()
     order = np.argsort(L)
     sample = sorted(set(order[np.linspace(0, n - 1, 4).astype(int)].tolist()))
     ref = ohead.predict(tokens, L, W, cfg, requests=sample)
     r = rel_err(gpu[sample], ref)
-    print("cfg3 sampled rel err", r.max(), "lengths", L[sample])
+    print(f"cfg3 {precision} sampled rel err", r.max(), "lengths", L[sample])
     assert r.max() <= PRED_RTOL
     starts = inputs.offsets(L)
     i = sample[-1]
