@@ -53,12 +53,23 @@ def parse():
                          "f4(iii) -- the precision that meets the north_star parity bars on every tested "
                          "input at bf16's speed, DESIGN.md R21), bf16 (default for the tiny d=32 encoder), or "
                          "fp8 E4M3 GEMMs (row f4(i); looser tolerance, DESIGN.md R20)")
+    ap.add_argument("--pooling", choices=["mean", "cls"], default="mean",
+                    help="mean (P:359, default) or CLS (P:138) pooling (DESIGN.md R2)")
+    ap.add_argument("--cls-last-layer", action="store_true",
+                    help="with --pooling cls: the last layer computes only the CLS rows (SURVEY.md 8f row f4(ii))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=12, help="requests in the oracle sample")
     ap.add_argument("--inflight", type=int, default=0,
                     help="total in-flight slots (BASELINE.json configs[4]: 65536). Each step re-predicts --n due "
                          "requests per GPU into this rank's slice of the table and selects over the whole table")
     return ap.parse_args()
+
+
+def encoder_cfg(args):
+    cfg = inputs.CONFIGS[args.config]
+    if args.pooling == "cls":
+        cfg = inputs.EncoderConfig(**{**cfg.to_dict(), "pooling": inputs.POOL_CLS})
+    return cfg
 
 
 def workload(args, rank: int):
@@ -96,7 +107,7 @@ def config_desc(args, T_local, world):
         "tokens_per_gpu_step": int(T_local),
         "lengths": args.lengths,
         "batch_cap": args.cap,
-        "pooling": "mean",
+        "pooling": args.pooling + (" (last layer on CLS rows only)" if args.cls_last_layer else ""),
         "precision": args.precision,
         "parallelism": f"request-sharded dp{world}" if world > 1 else "single GPU",
         "l2": "no flush: per-step working set (218 MB bf16 weights + >=0.5 GB activations) exceeds the 126 MB L2",
@@ -178,15 +189,21 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- roofline
-def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic_table: dict, fp8: bool = False):
+def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic_table: dict, fp8: bool = False,
+                    cls_last_layer: bool = False):
     """Dominant kernel class (largest share of device time) -> achieved vs measured peak."""
     H, F, nl = cfg.hidden, cfg.intermediate, cfg.num_layers
+    Lf = L.astype(np.float64)
+    # rows per launch, averaged over the step's launches (the CLS-only last layer runs n rows)
+    Tr = (T * (nl - 1) + len(L)) / nl if cls_last_layer else T
+    attn = 4.0 * H * (float(np.sum(Lf ** 2)) * (nl - 1) + float(np.sum(Lf))) / nl if cls_last_layer \
+        else 4.0 * H * float(np.sum(Lf ** 2))
     flops = {  # algorithmic FLOPs per launch
         "gemm_qkv": 2.0 * T * H * 3 * H,
-        "gemm_out": 2.0 * T * H * H,
-        "gemm_ffn1": 2.0 * T * H * F,
-        "gemm_ffn2": 2.0 * T * F * H,
-        "attention": 4.0 * H * float(np.sum(L.astype(np.float64) ** 2)),
+        "gemm_out": 2.0 * Tr * H * H,
+        "gemm_ffn1": 2.0 * Tr * H * F,
+        "gemm_ffn2": 2.0 * Tr * F * H,
+        "attention": attn,
     }
     bytes_ = {  # algorithmic HBM bytes per launch
         "layernorm": 10.0 * T * H,          # read u f32, write h f32 + h bf16
@@ -266,7 +283,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    cfg = inputs.CONFIGS[args.config]
+    cfg = encoder_cfg(args)
     W = inputs.make_weights(cfg, seed=0)
     L, gen, tokens = workload(args, 0)
     per_step = 2
@@ -305,7 +322,7 @@ def run_elis(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = inputs.CONFIGS[args.config]
+    cfg = encoder_cfg(args)
     W = inputs.make_weights(cfg, seed=0)
     st = torch.cuda.current_stream()
     d_ids = torch.empty(args.cap, dtype=torch.int32, device="cuda")
@@ -330,7 +347,8 @@ def run_elis(args):
         L = windows[0][5]
         tokens = windows[0][4]
         gen = gen_t[:n]
-        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision)
+        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision,
+                              cls_last_layer=args.cls_last_layer)
         d_table = torch.zeros(F, device="cuda")
         d_gen = torch.from_numpy(gen_t).cuda()
         for wt in windows:  # fill every slot's cached prediction once
@@ -349,7 +367,8 @@ def run_elis(args):
         L, gen, tokens = workload(args, rank)
         n, T = len(L), int(L.sum())
         T_roof = T
-        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision)
+        P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision,
+                              cls_last_layer=args.cls_last_layer)
         d_tok = torch.from_numpy(tokens).cuda()
         d_len = torch.from_numpy(L).cuda()
         d_gen = torch.from_numpy(gen).cuda()
@@ -446,7 +465,7 @@ def run_elis(args):
     if rank == 0:
         peaks = load_peaks()
         roof = kernel_roofline(prof, cfg, T_roof, L, peaks, load_traffic() if args.precision in ("bf16", "fp16") else {},
-                               fp8=args.precision == "fp8")
+                               fp8=args.precision == "fp8", cls_last_layer=args.cls_last_layer)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -481,6 +500,8 @@ def run_elis(args):
 
 def main():
     args = parse()
+    if args.cls_last_layer and args.pooling != "cls":
+        raise SystemExit("--cls-last-layer needs --pooling cls")
     if args.precision is None:
         args.precision = "fp16" if inputs.CONFIGS[args.config].head_dim == 64 else "bf16"
     if args.impl == "reference":

@@ -86,6 +86,9 @@ typedef struct {
   int32_t max_requests;       /* workspace capacity: max n per predict / select call          */
   int32_t device;             /* CUDA device ordinal                                          */
   int32_t precision;          /* elis_precision; default BF16                                 */
+  int32_t cls_last_layer;     /* 1 with pooling = CLS: the last layer computes only each      */
+                              /* request's CLS row (exact: nothing else reaches the head;     */
+                              /* SURVEY.md Sec. 8f row f4(ii)); needs head dim 64             */
 } elis_config;
 
 typedef struct elis_predictor elis_predictor;

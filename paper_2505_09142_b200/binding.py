@@ -35,7 +35,7 @@ class ElisConfig(ctypes.Structure):
                 ("num_layers", _i32), ("hidden", _i32), ("num_heads", _i32), ("intermediate", _i32),
                 ("ln_eps", _f32), ("pooling", _i32), ("head_layers", _i32), ("head_hidden", _i32),
                 ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32),
-                ("precision", _i32)]
+                ("precision", _i32), ("cls_last_layer", _i32)]
 
 
 class ElisStarvation(ctypes.Structure):
@@ -140,21 +140,23 @@ def _stream(stream):
 
 
 def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
-                head_predicts_total: bool = False, precision: str = "bf16") -> ElisConfig:
+                head_predicts_total: bool = False, precision: str = "bf16", cls_last_layer: bool = False) -> ElisConfig:
     return ElisConfig(ABI_VERSION, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
                       cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
-                      int(head_predicts_total), int(max_tokens), int(max_requests), int(device), PRECISION[precision])
+                      int(head_predicts_total), int(max_tokens), int(max_requests), int(device), PRECISION[precision],
+                      int(cls_last_layer))
 
 
 class Predictor:
     """Owner of one elis_predictor (device weights + workspaces)."""
 
     def __init__(self, cfg: inputs.EncoderConfig, flat_weights: np.ndarray, max_tokens: int, max_requests: int,
-                 device: int = 0, head_predicts_total: bool = False, precision: str = "bf16"):
+                 device: int = 0, head_predicts_total: bool = False, precision: str = "bf16",
+                 cls_last_layer: bool = False):
         L = lib()
         self.cfg = cfg
         self.precision = precision
-        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total, precision)
+        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total, precision, cls_last_layer)
         flat = np.ascontiguousarray(flat_weights, dtype=np.float32)
         need = L.elis_weight_count(ctypes.byref(self.c))
         if need != flat.size:

@@ -563,6 +563,95 @@ __global__ void __launch_bounds__(128, 4)
 #endif
 }
 
+// ============================================================================ CLS-only last layer
+// with CLS pooling only row 0 of each request leaves the
+// last encoder layer, so its attention needs one query row per (request, head) against the
+// request's L keys.  One 128-thread CTA per (head, request), fp32 throughout:
+//   s_j = q . k_j * log2(e) / sqrt(d)   (thread j mod 128 takes keys j, j + 128, ...)
+//   p_j = exp2(s_j - max s),  l = sum p_j
+//   ctx = sum_j p_j v_j / l            (thread t: column t mod 64, keys of parity t / 64)
+// Head 0's CTA also gathers the request's CLS residual row h32[cu_i] into the compact hres.
+// OUT: 0 bf16, 1 fp16, 2 E4M3(ctx_scale * ctx).
+template <int OUT>
+__global__ void __launch_bounds__(128) k_attention_cls(const uint16_t* __restrict__ qkv, const int32_t* __restrict__ cu,
+                                                       int nh, int Tp, int H, float scale_log2,
+                                                       const float* __restrict__ h32, uint16_t* __restrict__ ctx_c,
+                                                       float* __restrict__ hres_c, float ctx_scale) {
+  const int h = blockIdx.x, i = blockIdx.y;
+  const int start = __ldg(cu + i), L = __ldg(cu + i + 1) - start;
+  __shared__ float q[TD];
+  __shared__ float p[512];
+  __shared__ float red[8];
+  __shared__ float part[2][TD];
+  auto to_f = [](uint16_t b) {
+    if constexpr (OUT == 1) return __half2float(__ushort_as_half(b));
+    else return bf16_bits_to_f32(b);
+  };
+  const uint16_t* Q = qkv + (static_cast<size_t>(h) * Tp + start) * TD;
+  const uint16_t* K = qkv + (static_cast<size_t>(nh + h) * Tp + start) * TD;
+  const uint16_t* V = qkv + (static_cast<size_t>(2 * nh + h) * Tp + start) * TD;
+  const int t = threadIdx.x;
+  if (t < TD) q[t] = to_f(Q[t]);
+  if (h == 0)
+    for (int c = t; c < H; c += blockDim.x) hres_c[static_cast<size_t>(i) * H + c] = h32[static_cast<size_t>(start) * H + c];
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int j = t; j < L; j += blockDim.x) {
+    const uint4* kr = reinterpret_cast<const uint4*>(K + static_cast<size_t>(j) * TD);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < TD / 8; ++c) {
+      const uint4 v = __ldg(kr + c);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc = fmaf(q[8 * c + 2 * e], to_f(static_cast<uint16_t>(w[e] & 0xFFFFu)), acc);
+        acc = fmaf(q[8 * c + 2 * e + 1], to_f(static_cast<uint16_t>(w[e] >> 16)), acc);
+      }
+    }
+    p[j] = acc * scale_log2;
+    mx = fmaxf(mx, p[j]);
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0) red[warp_id()] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = t; j < L; j += blockDim.x) {
+    const float e = exp2f(p[j] - mx);
+    p[j] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  if (lane_id() == 0) red[4 + warp_id()] = sum;
+  __syncthreads();
+  const float l = (red[4] + red[5]) + (red[6] + red[7]);
+  const int col = t & (TD - 1), par = t >> 6;
+  float acc = 0.f;
+  for (int j = par; j < L; j += 2) acc = fmaf(p[j], to_f(V[static_cast<size_t>(j) * TD + col]), acc);
+  part[par][col] = acc;
+  __syncthreads();
+  if (t < TD) {
+    const float o = (part[0][t] + part[1][t]) / l;
+    const size_t dst = static_cast<size_t>(i) * H + h * TD + t;
+    if constexpr (OUT == 2) {
+      __shared__ float ob[TD];
+      ob[t] = o * ctx_scale;
+      __syncwarp();
+      if ((t & 3) == 0) {
+        // 4 E4M3 bytes per thread (t, t+1, t+2, t+3 of this warp)
+        reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(ctx_c) + static_cast<size_t>(i) * H + h * TD)[t >> 2] =
+            pack_e4m3x4(ob[t], ob[t + 1], ob[t + 2], ob[t + 3]);
+      }
+    } else if constexpr (OUT == 1) {
+      ctx_c[dst] = __half_as_ushort(__float2half_rn(o));
+    } else {
+      ctx_c[dst] = static_cast<uint16_t>(pack_bf16x2(o, 0.f) & 0xFFFFu);
+    }
+  }
+}
+
 }  // namespace
 
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
@@ -594,6 +683,23 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, num_heads, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens, int n, int H, int num_heads,
+                                 int64_t plane_rows, const float* h32, uint16_t* ctx_c, float* hres_c, int out_kind,
+                                 float ctx_scale, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (H / num_heads != TD) return cudaErrorInvalidValue;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(TD));
+  const dim3 grid(num_heads, n);
+  const int Tp = static_cast<int>(plane_rows);
+  switch (out_kind) {
+    case 0: k_attention_cls<0><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale); break;
+    case 1: k_attention_cls<1><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale); break;
+    case 2: k_attention_cls<2><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -96,6 +96,9 @@ bool config_valid(const elis_config* c, std::string* why) {
     return bad("precision");
   if (c->precision != ELIS_PREC_BF16 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
     return bad("FP8 / FP16 need head dim 64 and hidden, intermediate multiples of 256");
+  if (c->cls_last_layer != 0 && c->cls_last_layer != 1) return bad("cls_last_layer must be 0 or 1");
+  if (c->cls_last_layer && (c->pooling != ELIS_POOL_CLS || d != 64))
+    return bad("cls_last_layer needs pooling = CLS and head dim 64");
   return true;
 }
 
@@ -150,6 +153,11 @@ struct elis_predictor {
 
   // workspaces
   float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
+  // CLS-only last layer (cfg.cls_last_layer): compact per-request rows [max_requests, *]
+  float* hres_c = nullptr;
+  uint16_t *ctx_c = nullptr, *hb_c = nullptr, *g_c = nullptr;
+  int32_t* iota = nullptr;  // [max_requests + 1] = 0, 1, 2, ... (row i of the compact buffers)
+  GemmPlan c_out{}, c_ffn1{}, c_ffn2{};
   uint16_t *hb = nullptr, *qkv = nullptr, *ctx = nullptr, *g = nullptr;
   int32_t* cu = nullptr;
   AttnWork* work = nullptr;
@@ -190,6 +198,7 @@ struct elis_predictor {
 
   cudaStream_t last_stream = nullptr;
   int64_t last_T = 0;
+  int last_n = 0;
   uint32_t last_err_bits = 0;
 
   template <class T>
@@ -411,6 +420,17 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
   ALLOC(p->ctx, static_cast<size_t>(T) * H);
   ALLOC(p->g, static_cast<size_t>(T) * F);
+  if (cfg->cls_last_layer) {
+    ALLOC(p->hres_c, static_cast<size_t>(N) * H);
+    ALLOC(p->ctx_c, static_cast<size_t>(N) * H);
+    ALLOC(p->hb_c, static_cast<size_t>(N) * H);
+    ALLOC(p->g_c, static_cast<size_t>(N) * F);
+    ALLOC(p->iota, N + 1);
+    std::vector<int32_t> io(N + 1);
+    for (int i = 0; i <= N; ++i) io[i] = i;
+    if (cudaMemcpy(p->iota, io.data(), (N + 1) * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return cleanup_fail(ELIS_ERR_CUDA, "upload iota");
+  }
   ALLOC(p->cu, N + 1);
   p->tile_q = attn_tile_q(H / cfg->num_heads);
   p->max_tiles = attn_work_capacity(T, N, p->tile_q);
@@ -461,6 +481,25 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
          gemm_plan_set_ln(&L.p_ffn2, p->hb, L.ln2g, L.ln2b, cfg->ln_eps, T);
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
+  if (cfg->cls_last_layer) {  // the last layer's out-proj / FFN over the compact CLS rows
+    Layer& L = p->layers.back();
+    bool ok;
+    if (f8)
+      ok = make_gemm_plan_f8(&p->c_out, p->ctx_c, N, L.wo, L.so, L.bo, p->hres_c, p->hres_c, 0, H, H,
+                             EPI_BIAS_RESID_LN, kF8ScaleHidden) &&
+           make_gemm_plan_f8(&p->c_ffn1, p->hb_c, N, L.w1, L.s1, L.b1, nullptr, p->g_c, 0, F, H, EPI_BIAS_GELU_BF16,
+                             kF8ScaleGelu) &&
+           make_gemm_plan_f8(&p->c_ffn2, p->g_c, N, L.w2, L.s2, L.b2, p->hres_c, p->hres_c, 0, H, F,
+                             EPI_BIAS_RESID_LN, kF8ScaleHidden);
+    else
+      ok = make_gemm_plan(&p->c_out, p->ctx_c, N, L.wo, L.bo, p->hres_c, p->hres_c, 0, H, H, EPI_BIAS_RESID_LN) &&
+           make_gemm_plan(&p->c_ffn1, p->hb_c, N, L.w1, L.b1, nullptr, p->g_c, 0, F, H, EPI_BIAS_GELU_BF16) &&
+           make_gemm_plan(&p->c_ffn2, p->g_c, N, L.w2, L.b2, p->hres_c, p->hres_c, 0, H, F, EPI_BIAS_RESID_LN);
+    if (f16) p->c_out.f16 = p->c_ffn1.f16 = p->c_ffn2.f16 = 1;
+    ok = ok && gemm_plan_set_ln(&p->c_out, p->hb_c, L.ln1g, L.ln1b, cfg->ln_eps, N) &&
+         gemm_plan_set_ln(&p->c_ffn2, p->hb_c, L.ln2g, L.ln2b, cfg->ln_eps, N);
+    if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled (CLS last layer) failed");
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "create sync");
 #undef ALLOC
   *out = p;
@@ -483,6 +522,7 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   const int64_t T_cap = c.max_tokens;  // rows of each head-major qkv plane
   p->last_stream = st;
   p->last_T = total_tokens;
+  p->last_n = n;
 
   LAUNCH(p, PC_META, st,
          launch_meta(lengths, n, total_tokens, c.max_position, p->cu, p->work, p->num_work, p->err, p->tile_q, st));
@@ -490,10 +530,24 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
          launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
                          p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err,
                          c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, c.precision == ELIS_PREC_FP16, st));
+  const float f8_ctx = c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f;
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
+    if (c.cls_last_layer && l == c.num_layers - 1) {
+      // CLS pooling: only row 0 of each request reaches the head, so the last layer's
+      // attention / out-proj / FFN run on n compact rows
+      const int kind = c.precision == ELIS_PREC_FP8 ? 2 : c.precision == ELIS_PREC_FP16 ? 1 : 0;
+      LAUNCH(p, PC_ATTN, st,
+             launch_attention_cls(p->qkv, p->cu, n, H, c.num_heads, T_cap, p->h32, p->ctx_c, p->hres_c, kind, f8_ctx,
+                                  st));
+      p->c_out.args.M = p->c_ffn1.args.M = p->c_ffn2.args.M = n;
+      LAUNCH(p, PC_OUT, st, launch_gemm(p->c_out, p->num_sms, st));
+      LAUNCH(p, PC_FFN1, st, launch_gemm(p->c_ffn1, p->num_sms, st));
+      LAUNCH(p, PC_FFN2, st, launch_gemm(p->c_ffn2, p->num_sms, st));
+      break;
+    }
     LAUNCH(p, PC_ATTN, st,
            launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
                             c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, st));
@@ -501,7 +555,10 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
   }
-  LAUNCH(p, PC_POOL, st, launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
+  if (c.cls_last_layer)  // row i of the compact buffer is request i's CLS row
+    LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st));
+  else
+    LAUNCH(p, PC_POOL, st, launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
   const float* x = p->pooled;
   float* bufs[2] = {p->z0, p->z1};
   const int nl = c.head_layers;
@@ -751,6 +808,8 @@ elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* 
   const int64_t need = p->last_T * p->cfg.hidden;
   if (count < need) return fail(ELIS_ERR_INVALID_ARG, "dst too small");
   CUDA_TRY(cudaMemcpyAsync(dst, p->h32, need * 4, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  if (p->cfg.cls_last_layer)  // the final CLS rows live in the compact buffer
+    CUDA_TRY(launch_scatter_rows(p->hres_c, p->cu, p->last_n, p->cfg.hidden, dst, static_cast<cudaStream_t>(stream)));
   return ELIS_OK;
 }
 

@@ -101,7 +101,16 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
                              int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st);
 
+// CLS-only last layer: per (request, head) the attention of the CLS
+// query row (row cu[i]) over the request's keys, from the head-major qkv planes; writes the
+// compact ctx_c [n, H] (out_kind 0 bf16, 1 fp16, 2 E4M3(ctx_scale x)) and gathers the CLS
+// residual rows h32[cu[i]] into hres_c [n, H].  Head dim 64.
+cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens, int n, int H, int num_heads,
+                                 int64_t plane_rows, const float* h32, uint16_t* ctx_c, float* hres_c, int out_kind,
+                                 float ctx_scale, cudaStream_t st);
+
 // ---- pooling + regression head (head.cu)
+cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, float* dst, cudaStream_t st);
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
                         float* pooled, cudaStream_t st);
 cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,

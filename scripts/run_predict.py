@@ -27,8 +27,12 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print per-kernel ms from the library profiler")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8", "fp16"])
+    ap.add_argument("--pooling", default="mean", choices=["mean", "cls"])
+    ap.add_argument("--cls-last-layer", action="store_true", help="CLS pooling: last layer on CLS rows only")
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
+    if a.pooling == "cls":
+        cfg = inputs.EncoderConfig(**{**cfg.to_dict(), "pooling": inputs.POOL_CLS})
     if a.lengths == "trace":
         L = inputs.trace_lengths(a.n, seed=0)[0]
     elif a.lengths == "uniform":
@@ -38,7 +42,7 @@ def main():
     tok = inputs.make_tokens(L, seed=0)
     T = int(L.sum())
     p = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg)), max_tokens=T, max_requests=a.n,
-                         precision=a.precision)
+                         precision=a.precision, cls_last_layer=a.cls_last_layer)
     dev = torch.device("cuda:0")
     t_tok = torch.from_numpy(tok).to(dev)
     t_len = torch.from_numpy(L.astype(np.int32)).to(dev)

@@ -97,3 +97,15 @@ def test_precision_validation():
     bad = binding.make_config(inputs.CONFIGS["base"], 1024, 16)
     bad.precision = 7
     assert L.elis_weight_count(ctypes.byref(bad)) == 0
+
+
+def test_cls_last_layer_validation():
+    """The CLS-only last layer requires CLS pooling and head dim 64."""
+    L = binding.lib()
+    cls_cfg = inputs.EncoderConfig(**{**inputs.CONFIGS["base"].to_dict(), "pooling": inputs.POOL_CLS})
+    ok = binding.make_config(cls_cfg, 1024, 16, cls_last_layer=True)
+    assert L.elis_weight_count(ctypes.byref(ok)) > 0
+    mean = binding.make_config(inputs.CONFIGS["base"], 1024, 16, cls_last_layer=True)
+    assert L.elis_weight_count(ctypes.byref(mean)) == 0
+    tiny = inputs.EncoderConfig(**{**inputs.CONFIGS["tiny"].to_dict(), "pooling": inputs.POOL_CLS})
+    assert L.elis_weight_count(ctypes.byref(binding.make_config(tiny, 1024, 16, cls_last_layer=True))) == 0
