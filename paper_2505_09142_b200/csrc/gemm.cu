@@ -56,8 +56,14 @@ namespace {
 
 constexpr int BM = 128;  // rows per CTA (256 per pair)
 constexpr int BK = 64;
-constexpr int kEpiWarps = 8;
-constexpr int kGemmThreads = 128 + kEpiWarps * 32;  // 4 control warps + 8 epilogue warps
+// Epilogue warps: 8, except the FP8 GELU epilogue: with the E4M3 mainloop twice as fast it is the
+// bound of FFN1 and runs 16 warps (<= 96 registers each; measured FFN1 1.84 -> 1.65 ms per cfg2
+// step, while 16 warps made the bf16 / fp16 QKV and FFN1 3-5% slower).
+template <int EPI, int PREC>
+constexpr int epi_warps() { return (PREC == 1 && EPI == EPI_BIAS_GELU_BF16) ? 16 : 8; }
+template <int EPI, int PREC>
+constexpr int gemm_threads() { return 128 + epi_warps<EPI, PREC>() * 32; }  // 4 control warps + epilogue warps
+constexpr int kMaxEpiWarps = 16;
 constexpr int kMaxCluster = 4;                       // max N-tiles (pairs) per LN row
 constexpr int kBox = 32;                             // epilogue TMA boxes: 32 rows x 32 columns
 
@@ -68,25 +74,25 @@ struct GemmCfg {
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int CHUNKS_PER_WARP = BN / 64;   // 32-column chunks per epilogue warp
 };
 // Shared-memory plan per epilogue kind.  DEEP (long-K residual GEMMs, e.g. FFN2: the mainloop
 // dominates) trades the second residual slot of each warp for a fourth operand stage.
-template <int BN, int EPI, bool DEEP>
+template <int BN, int EPI, bool DEEP, int PREC>
 struct SmemPlan {
   static constexpr bool LN = EPI == EPI_BIAS_RESID_LN;
   static constexpr bool RES = LN || EPI == EPI_BIAS_RESID_F32;
   static constexpr bool OUT_F32 = RES;                 // f32 staging (4 KB per warp)
   static constexpr bool OUT_BF16 = LN || !RES;         // bf16 staging (2 KB per warp)
-  static constexpr int NSTG = RES ? 1 : 2;             // staging buffers per warp
+  static constexpr int EW = epi_warps<EPI, PREC>();
+  static constexpr int NSTG = (RES || EW == 16) ? 1 : 2;  // staging buffers per warp
   static constexpr int NRES = (RES && DEEP) ? 1 : 2;   // residual slots per warp
   static constexpr int STAGES = RES ? (DEEP ? 4 : 3) : 5;
   static constexpr int RES_SLOT = kBox * kBox * 4;     // 4 KB fp32 residual box
-  static constexpr int RES_BYTES = RES ? kEpiWarps * NRES * RES_SLOT : 0;
+  static constexpr int RES_BYTES = RES ? EW * NRES * RES_SLOT : 0;
   static constexpr int STG_F32 = kBox * kBox * 4;      // 4 KB
   static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
   static constexpr int STG_WARP = NSTG * ((OUT_F32 ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
-  static constexpr int STG_BYTES = kEpiWarps * STG_WARP;
+  static constexpr int STG_BYTES = EW * STG_WARP;
   // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta/colscale[256] f32
   static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 4 * 256 * 4;
   static constexpr int SMEM_BYTES = STAGES * GemmCfg<BN>::STAGE_BYTES + RES_BYTES + STG_BYTES + AUX_BYTES + 1024;
@@ -98,10 +104,11 @@ struct SmemPlan {
 // 2.6e-5 (scripts/fit_gelu.py), < 1/75 of the bf16 rounding of the output this epilogue
 // writes.  10 instructions incl. 2 MUFU instead of ~28 for erff (the FFN1 epilogue is
 // instruction-issue bound).
-#ifdef ELIS_GELU_TANH
 // Same minimax sigmoid form evaluated as x sigmoid(y) = 0.5 x (1 + tanh(y / 2)): one MUFU
-// (tanh.approx) instead of two; error measured by scripts/gelu_acc.cu.
-ELIS_DEV float gelu_fast(float x) {
+// (tanh.approx) instead of two, max |error| 3.0e-5 (scripts/gelu_acc.cu).  Used by the FP8 FFN1
+// epilogue (MUFU-heavy once the E4M3 mainloop halves: 1.65 -> 1.53 ms per cfg2 step); the 16-bit
+// paths keep the two-MUFU form, which measured faster there.
+ELIS_DEV float gelu_tanh_form(float x) {
   constexpr float a0 = 0.5f * 1.5950205882421884f, a1 = 0.5f * 0.07400664121448398f,
                   a2 = -0.5f * 0.0007022165804436097f;
   const float xc = fminf(fmaxf(x, -9.0f), 9.0f);
@@ -112,7 +119,6 @@ ELIS_DEV float gelu_fast(float x) {
   const float h = 0.5f * x;
   return fmaf(h, t, h);
 }
-#else
 ELIS_DEV float gelu_fast(float x) {
   constexpr float kL2E = 1.4426950408889634f;
   constexpr float c0 = -1.5950205882421884f * kL2E, c1 = -0.07400664121448398f * kL2E,
@@ -125,7 +131,6 @@ ELIS_DEV float gelu_fast(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
   return x * r;
 }
-#endif
 
 // Chan et al. merge of (count, mean, M2) partial statistics.
 ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
@@ -158,17 +163,19 @@ ELIS_DEV void stage_e4m3_row(uint8_t* b, int lane, const float (&v)[32], float s
 
 // PREC: 0 bf16 operands, 1 E4M3 operands (kind::f8f6f4), 2 fp16 operands (16-bit outputs in fp16)
 template <int BN, int EPI, bool DEEP, int PREC>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
               const __grid_constant__ CUtensorMap tmOb, const GemmArgs args) {
   using C = GemmCfg<BN>;
-  using SP = SmemPlan<BN, EPI, DEEP>;
+  using SP = SmemPlan<BN, EPI, DEEP, PREC>;
   constexpr int NRES = SP::NRES;
   constexpr bool LN = SP::LN;
   constexpr bool RES = SP::RES;
   constexpr int STAGES = SP::STAGES;
   constexpr bool F8 = PREC == 1;
+  constexpr int EW = SP::EW;                 // epilogue warps
+  static_assert(!LN || EW == 8, "the LN statistics exchange assumes two column halves per CTA");
   constexpr bool F16 = PREC == 2;
   // K elements per 128-byte operand row: 64 bf16 or 128 E4M3 (4 MMAs of K 16 / K 32 either way)
   constexpr int BKE = F8 ? 2 * BK : BK;
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;    // LN: stats slots filled by every CTA of the row group
   uint64_t* rfull = sfull + 2;     // [warp][2]: residual slot landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2 * kEpiWarps);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 2 * EW);
   float2* stats = reinterpret_cast<float2*>(aux + 512);    // [2][kMaxCluster][128]
   float2* part = stats + 2 * kMaxCluster * 128;             // [2 halves][128]
   float* sbias = reinterpret_cast<float*>(part + 2 * 128);   // [256]
@@ -223,10 +230,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * kEpiWarps);  // one arrive per epilogue warp of both CTAs (leader's copy used)
+      mbar_init(&tempty[a], 2 * EW);  // one arrive per epilogue warp of both CTAs (leader's copy used)
       mbar_init(&sfull[a], 4 * cpairs);      // one arrive per half-0 epilogue warp of every row peer
     }
-    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&rfull[i], 1);
+    for (int i = 0; i < 2 * EW; ++i) mbar_init(&rfull[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -297,10 +304,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (each CTA: its 128 rows; warp: 32 rows x BN/2 columns)
-    constexpr int CH = C::CHUNKS_PER_WARP;
+    constexpr int CPW = BN / (EW / 4);   // tile columns per epilogue warp
+    constexpr int CH = CPW / 32;         // 32-column chunks per epilogue warp
     const int ew = warp - 4;             // 0..7
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = ew >> 2;            // which half of the tile's columns
+    const int half = ew >> 2;            // which column part of the tile (a half when EW = 8)
     const int row_in_tile = q * 32 + lane;
     const int etid = ew * 32 + lane;     // 0..255
     uint8_t* rslot = sRes + ew * NRES * SP::RES_SLOT;
@@ -350,7 +358,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     };
     if constexpr (LN) {
       stage_vectors(pair_in_cluster);
-      named_bar_sync(1, kEpiWarps * 32);
+      named_bar_sync(1, EW * 32);
     }
     int it = 0;
     const long long gepi = GT_CLK();
@@ -361,16 +369,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       const int row0 = m * 2 * BM + hrow * BM + q * 32;   // first row of this warp's block
-      const int cbase = half * (BN / 2);                   // first tile column of this warp
+      const int cbase = half * CPW;                        // first tile column of this warp
       if (RES && !res_prefetched) {       // residual does not depend on the MMA: fetch it now
 #pragma unroll
         for (int c = 0; c < NRES && c < CH; ++c) load_res(row0, n * BN + cbase + c * 32, c);
       }
       res_prefetched = false;
       if constexpr (!LN) {
-        named_bar_sync(1, kEpiWarps * 32);  // previous tile's readers of sbias are done
+        named_bar_sync(1, EW * 32);  // previous tile's readers of sbias are done
         stage_vectors(n);
-        named_bar_sync(1, kEpiWarps * 32);
+        named_bar_sync(1, EW * 32);
       }
       const bool gt_me = (warp == 4 && lane == 0);
       long long g0 = GT_CLK();
@@ -443,7 +451,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             if constexpr (EPI == EPI_BIAS_GELU_BF16) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
+              for (int j = 0; j < 32; ++j) v[j] = F8 ? gelu_tanh_form(v[j]) : gelu_fast(v[j]);
             }
             if constexpr (F8 && EPI == EPI_BIAS_GELU_BF16) {
               stage_e4m3_row(b, lane, v, args.out_scale);
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int slot = it & 1;
         const uint32_t sph = (it >> 1) & 1;
         part[half * 128 + row_in_tile] = make_float2(st_mean, st_m2);
-        named_bar_sync(2, kEpiWarps * 32);
+        named_bar_sync(2, EW * 32);
         if (half == 0) {
           // this CTA's statistics over its BN columns -> every CTA holding the same rows
           float cn = st_n, cmean = st_mean, cm2 = st_m2;
@@ -561,7 +569,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 template <int BN, int EPI, bool DEEP, int PREC = 0>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
-  using SP = SmemPlan<BN, EPI, DEEP>;
+  using SP = SmemPlan<BN, EPI, DEEP, PREC>;
   auto kern = k_gemm_tc<BN, EPI, DEEP, PREC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -572,7 +580,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   const int csize = 2 * cpairs;
   if (cpairs > kMaxCluster) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(gemm_threads<EPI, PREC>());
   cfg.dynamicSmemBytes = SP::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -25,7 +25,8 @@ NAMES = ["prod wait(empty)", "mma wait(acc free)", "mma wait(smem full)", "mma s
 
 
 def main():
-    M = int(sys.argv[1]) if len(sys.argv) > 1 else 43296
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    M = int(args[0]) if args else 43296
     H, F = 768, 3072
     dev = torch.device("cuda")
     lib = binding.lib()
@@ -51,6 +52,21 @@ def main():
                                                       torch.ones(H, device=dev), torch.zeros(H, device=dev), 1e-12,
                                                       torch.empty(M, H, dtype=torch.bfloat16, device=dev)),
     }
+    if "--fp8" in sys.argv:  # E4M3 operands (kind::f8f6f4) on the same shapes
+        def f8(*shape, scale=4.0):
+            return (torch.randn(*shape, generator=g) * scale).to(torch.float8_e4m3fn).view(torch.uint8).to(dev)
+        h8, g8 = f8(M, H), f8(M, F)
+        cs = lambda n: torch.full((n,), 1e-3, device=dev)
+        shapes = {
+            "qkv fp8": lambda: binding.op_gemm_f8(h8, f8(3 * H, H), cs(3 * H), rnd(3 * H).float(),
+                                                 torch.empty(M, 3 * H, dtype=torch.bfloat16, device=dev), 0),
+            "ffn1 fp8 (GELU, e4m3 out)": lambda: binding.op_gemm_f8(h8, f8(F, H), cs(F), rnd(F).float(),
+                                                                   torch.empty(M, F, dtype=torch.uint8, device=dev),
+                                                                   1, 16.0),
+            "ffn2+LN fp8": lambda: binding.op_gemm_ln_f8(g8, f8(H, F), cs(H), rnd(H).float(), rnd(M, H).float(),
+                                                        torch.ones(H, device=dev), torch.zeros(H, device=dev),
+                                                        1e-12, torch.empty(M, H, dtype=torch.uint8, device=dev), 8.0),
+        }
     clk_ghz = None
     for name, call in shapes.items():
         call()
