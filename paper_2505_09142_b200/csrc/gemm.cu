@@ -76,7 +76,9 @@ struct GemmCfg {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
 // Shared-memory plan per epilogue kind.  DEEP (long-K residual GEMMs, e.g. FFN2: the mainloop
-// dominates) trades the second residual slot of each warp for a fourth operand stage.
+// dominates and the epilogue has slack) keeps one residual slot per warp and, for LN, stages the
+// fp32 output in that slot too (the next tile's residual is fetched once the slot's store has
+// been read): the freed 64 KB buy a fourth and a fifth operand stage.
 template <int BN, int EPI, bool DEEP, int PREC>
 struct SmemPlan {
   static constexpr bool LN = EPI == EPI_BIAS_RESID_LN;
@@ -86,12 +88,13 @@ struct SmemPlan {
   static constexpr int EW = epi_warps<EPI, PREC>();
   static constexpr int NSTG = (RES || EW == 16) ? 1 : 2;  // staging buffers per warp
   static constexpr int NRES = (RES && DEEP) ? 1 : 2;   // residual slots per warp
-  static constexpr int STAGES = RES ? (DEEP ? 4 : 3) : 5;
+  static constexpr bool F32_IN_RES = LN && DEEP;        // fp32 output staged in the residual slot
+  static constexpr int STAGES = RES ? (DEEP ? (F32_IN_RES ? 5 : 4) : 3) : 5;
   static constexpr int RES_SLOT = kBox * kBox * 4;     // 4 KB fp32 residual box
   static constexpr int RES_BYTES = RES ? EW * NRES * RES_SLOT : 0;
   static constexpr int STG_F32 = kBox * kBox * 4;      // 4 KB
   static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
-  static constexpr int STG_WARP = NSTG * ((OUT_F32 ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
+  static constexpr int STG_WARP = NSTG * (((OUT_F32 && !F32_IN_RES) ? STG_F32 : 0) + (OUT_BF16 ? STG_BF16 : 0));
   static constexpr int STG_BYTES = EW * STG_WARP;
   // barriers (512) + LN stats[2][kMaxCluster][128] f2 + part[2][128] f2 + bias/gamma/beta/colscale[256] f32
   static constexpr int AUX_BYTES = 512 + 2 * kMaxCluster * 128 * 8 + 2 * 128 * 8 + 4 * 256 * 4;
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
     // residual box (32 rows x 32 columns at col0, row0) -> slot c & 1 (lane 0 issues)
     auto load_res = [&](int row0, int col0, int c) {
       if (lane == 0) {
+        if constexpr (SP::F32_IN_RES) tma_store_wait_read<0>();  // the slot's output store has read it
         fence_proxy_async_smem();   // slot previously read through the generic proxy
         mbar_arrive_expect_tx(&rbar[c % NRES], SP::RES_SLOT);
         tma_load_2d(rslot + (c % NRES) * SP::RES_SLOT, &tmR, &rbar[c % NRES], col0, row0);
@@ -342,13 +346,14 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
       __syncwarp();
       return b;
     };
-    auto issue_store = [&](uint8_t* b, int row0, int col0) {
+    // b: the staging of this store group; the fp32 box is read from b32 (b, or the residual slot)
+    auto issue_store = [&](uint8_t* b, int row0, int col0, uint8_t* b32 = nullptr) {
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (SP::OUT_F32) tma_store_2d(&tmO, b, col0, row0);
+        if constexpr (SP::OUT_F32) tma_store_2d(&tmO, b32 ? b32 : b, col0, row0);
         if constexpr (SP::OUT_BF16) {
-          if constexpr (SP::OUT_F32) tma_store_2d(&tmOb, b + SP::STG_F32, col0, row0);
+          if constexpr (SP::OUT_F32) tma_store_2d(&tmOb, SP::F32_IN_RES ? b : b + SP::STG_F32, col0, row0);
           else if (args.out_head_major) tma_store_3d(&tmO, b, col0 & 63, row0, col0 >> 6);
           else tma_store_2d(&tmO, b, col0, row0);
         }
@@ -470,8 +475,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
       if constexpr (LN) {
         tc_wait_st();
         // pass 1 has consumed this tile's residual: start the next tile's first boxes now so the
-        // loads overlap the statistics exchange and pass 2
-        if (t + ncl < num_iter_tiles) {
+        // loads overlap the statistics exchange and pass 2 (not when pass 2 stages in the slot)
+        if (!SP::F32_IN_RES && t + ncl < num_iter_tiles) {
           int m2, n2;
           tile_mn(t + ncl, m2, n2);
           const int row0n = m2 * 2 * BM + hrow * BM + q * 32;
@@ -525,12 +530,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
             y[j + 2] = (__uint_as_float(r[c & 1][j + 2]) - tmean) * rstd * g.z + be.z;
             y[j + 3] = (__uint_as_float(r[c & 1][j + 3]) - tmean) * rstd * g.w + be.w;
           }
-          uint8_t* b = next_stage();
+          uint8_t* b = next_stage();   // NSTG = 1: every earlier store (incl. from the slot) has read
+          uint8_t* b32 = SP::F32_IN_RES ? rslot : b;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            *reinterpret_cast<float4*>(b + sw128_off(lane, k)) =
+            *reinterpret_cast<float4*>(b32 + sw128_off(lane, k)) =
                 make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
-          uint8_t* bb = b + SP::STG_F32;
+          uint8_t* bb = SP::F32_IN_RES ? b : b + SP::STG_F32;
           if constexpr (F8) {
             stage_e4m3_row(bb, lane, y, args.out_scale);
           } else {
@@ -540,7 +546,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
                   make_uint4(pack16x2<F16>(y[8 * k + 0], y[8 * k + 1]), pack16x2<F16>(y[8 * k + 2], y[8 * k + 3]),
                              pack16x2<F16>(y[8 * k + 4], y[8 * k + 5]), pack16x2<F16>(y[8 * k + 6], y[8 * k + 7]));
           }
-          issue_store(b, row0, col0);
+          issue_store(b, row0, col0, b32);
         }
         if (gt_me) GT_ADD(7, GT_CLK() - g1);
       }
