@@ -59,6 +59,10 @@ def parse():
                     help="with --pooling cls: the last layer computes only the CLS rows (SURVEY.md 8f row f4(ii))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=12, help="requests in the oracle sample")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: exchange of the local top-cap candidates -- peer: one fused kernel storing them "
+                         "into every rank's CUDA-IPC-mapped region over NVLink (elis_peer_attach); nccl: "
+                         "ncclAllGather between pack / merge kernels (elis_dist_attach)")
     ap.add_argument("--inflight", type=int, default=0,
                     help="total in-flight slots (BASELINE.json configs[4]: 65536). Each step re-predicts --n due "
                          "requests per GPU into this rank's slice of the table and selects over the whole table")
@@ -94,11 +98,11 @@ def config_desc(args, T_local, world):
         wl = (f"cfg5 due-set: {args.config} encoder, {args.inflight} in-flight requests ({args.inflight // world} "
               f"per GPU); each iteration re-predicts {args.n} due requests per GPU into the in-flight table and "
               f"selects batch_cap {args.cap} over all {args.inflight} cached keys"
-              + (" (local top-cap + NCCL all-gather + merge)" if world > 1 else ""))
+              + (f" (local top-cap + {args.transport_used} exchange + merge)" if world > 1 else ""))
     else:
         wl = (f"cfg{ {'tiny': 1, 'base': 2, 'large': 3}[args.config] }: {args.config} encoder re-predicting "
               f"{args.n} in-flight requests per GPU ({args.lengths} lengths) + ISRTF select batch_cap "
-              f"{args.cap}" + (f" over {world}x{args.n} via NCCL all-gather" if world > 1 else ""))
+              f"{args.cap}" + (f" over {world}x{args.n} via {args.transport_used} exchange of local top-cap" if world > 1 else ""))
     return {
         "workload": wl,
         "encoder": args.config,
@@ -110,6 +114,7 @@ def config_desc(args, T_local, world):
         "pooling": args.pooling + (" (last layer on CLS rows only)" if args.cls_last_layer else ""),
         "precision": args.precision,
         "parallelism": f"request-sharded dp{world}" if world > 1 else "single GPU",
+        **({"transport": args.transport_used} if world > 1 else {}),
         "l2": "no flush: per-step working set (218 MB bf16 weights + >=0.5 GB activations) exceeds the 126 MB L2",
     }
 
@@ -380,11 +385,29 @@ def run_elis(args):
                 P.isrtf_select_dist(d_pred, d_gen, rank * n, args.cap, d_ids, out_count=d_cnt, stream=st)
             else:
                 P.isrtf_select(d_pred, d_gen, args.cap, d_ids, out_count=d_cnt, stream=st)
+    args.transport_used = "none"
     if world > 1:
-        uid = binding.nccl_unique_id() if rank == 0 else bytes(128)
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        P.dist_attach(rank, world, obj[0])
+        ok = 0
+        if args.transport == "peer":
+            # symmetric regions mapped through CUDA IPC; every rank must agree on the transport
+            try:
+                h = P.peer_export(rank, world)
+                hs = [None] * world
+                dist.all_gather_object(hs, h)
+                P.peer_attach(hs)
+                ok = 1
+            except binding.ElisError as e:
+                print(f"[rank {rank}] peer transport unavailable: {e}", file=sys.stderr)
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            args.transport_used = "peer (NVLink stores + epoch flags, fused select kernel)"
+        else:
+            uid = binding.nccl_unique_id() if rank == 0 else bytes(128)
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            P.dist_attach(rank, world, obj[0])   # the last attach wins: NCCL transport
+            args.transport_used = "nccl all-gather"
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -50,7 +50,8 @@ typedef enum {
   ELIS_ERR_OOM = 4,                /* device allocation failed                        */
   ELIS_ERR_CUDA = 5,               /* a CUDA runtime/driver call failed               */
   ELIS_ERR_NCCL = 6,               /* an NCCL call failed                             */
-  ELIS_ERR_DEVICE_INPUT = 7        /* sticky device-detected input error (see above)  */
+  ELIS_ERR_DEVICE_INPUT = 7,       /* sticky device-detected input error (see above)  */
+  ELIS_ERR_PEER_TIMEOUT = 8        /* sticky: a peer-memory select waited > 10 s for a rank */
 } elis_status;
 
 typedef enum { ELIS_POOL_MEAN = 0, ELIS_POOL_CLS = 1 } elis_pooling;   /* P:359 / P:138 */
@@ -208,6 +209,26 @@ elis_status elis_dist_attach(elis_predictor* p, int32_t rank, int32_t world, con
 elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const int32_t* generated,
                                    int32_t n_local, int32_t global_offset, int32_t batch_cap,
                                    const elis_preempt* preempt, int32_t* out_ids, void* stream);
+
+/* ---- multi-GPU over peer memory (NVLink 5 / NVSwitch loads and stores, no NCCL) ----------
+ * The same global select as elis_isrtf_select_dist (SURVEY.md Sec. 8a row a13, 8e "B200-native
+ * stretch"), with the exchange done by ONE kernel: each rank's local top-cap candidates
+ * (u64 key + global id) are stored directly into every rank's symmetric receive region through
+ * CUDA-IPC-mapped pointers and published by an epoch flag (st.release.sys); each rank then
+ * acquires all `world` flags and runs the identical merge.  Results are bit-identical to the
+ * NCCL transport.  Setup, once per predictor:
+ *   1. elis_peer_export(p, rank, world, handle): allocates this rank's region (~0.8 MB) and
+ *      writes its 64-byte cudaIpcMemHandle_t to `handle` (HOST memory);
+ *   2. the caller all-gathers the handles in rank order (e.g. torch.distributed);
+ *   3. elis_peer_attach(p, handles): maps every other rank's region (HOST array world x 64 B).
+ * From then on elis_isrtf_select_dist uses this transport.  Every rank must make the same
+ * sequence of elis_isrtf_select_dist calls (like a collective); world <= 8.  A rank that never
+ * arrives makes the waiting ranks give up after 10 s with the sticky ELIS_ERR_PEER_TIMEOUT
+ * (outputs: count 0, ids -1).  elis_peer_attach_local wires predictors that live in ONE process
+ * (peers[r] = rank r; devices may repeat -- tests -- or differ, with peer access enabled). */
+elis_status elis_peer_export(elis_predictor* p, int32_t rank, int32_t world, void* out_handle64);
+elis_status elis_peer_attach(elis_predictor* p, const void* handles);
+elis_status elis_peer_attach_local(elis_predictor* const* peers, int32_t world);
 
 /* ---- end-to-end convenience (HOST buffers) ----------------------------------------------
  * One scheduling iteration from host memory: H2D copy of tokens/lengths/generated

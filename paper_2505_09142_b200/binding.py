@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 ELIS_OK = 0
 ABI_VERSION = 3  # include/elis.h ELIS_ABI_VERSION
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
-          6: "nccl", 7: "device input"}
+          6: "nccl", 7: "device input", 8: "peer timeout"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
 EPI_BIAS_BF16, EPI_BIAS_GELU_BF16, EPI_BIAS_RESID_F32 = 0, 1, 2
 PRECISION = {"bf16": 0, "fp8": 1, "fp16": 2}  # elis_precision
@@ -86,6 +86,9 @@ def lib():
         "elis_nccl_unique_id": (_i32, [_vp]),
         "elis_dist_attach": (_i32, [_vp, _i32, _i32, _vp]),
         "elis_isrtf_select_dist": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+        "elis_peer_export": (_i32, [_vp, _i32, _i32, _vp]),
+        "elis_peer_attach": (_i32, [_vp, _vp]),
+        "elis_peer_attach_local": (_i32, [_vp, _i32]),
         "elis_assign_nodes": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp]),
         "elis_isrtf_select_nodes": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
         "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp,
@@ -212,6 +215,17 @@ class Predictor:
         buf = ctypes.create_string_buffer(bytes(unique_id), 128)
         check(lib().elis_dist_attach(self.h, rank, world, buf), "elis_dist_attach")
 
+    def peer_export(self, rank: int, world: int) -> bytes:
+        """Allocate this rank's peer region; return its 64-byte CUDA IPC handle."""
+        buf = ctypes.create_string_buffer(64)
+        check(lib().elis_peer_export(self.h, int(rank), int(world), buf), "elis_peer_export")
+        return buf.raw
+
+    def peer_attach(self, handles: list[bytes]):
+        """Map every rank's region (handles in rank order, as all-gathered by the caller)."""
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * len(handles))
+        check(lib().elis_peer_attach(self.h, buf), "elis_peer_attach")
+
     def isrtf_select_dist(self, pred, generated, global_offset: int, batch_cap: int, out_ids, policy=POLICY_ISRTF,
                           allow_preempt=True, order=None, running=None, out_preempted=None, out_count=None,
                           out_nan_count=None, stream=None):
@@ -255,6 +269,12 @@ class Predictor:
         cnt = (ctypes.c_int64 * cap)()
         k = lib().elis_profile_read(self.h, names, ms, cnt, cap)
         return {names[i].decode(): (ms[i], cnt[i]) for i in range(min(k, cap)) if cnt[i] > 0}
+
+
+def peer_attach_local(predictors: list["Predictor"]):
+    """Wire predictors of ONE process as ranks 0..world-1 of the peer-memory transport."""
+    arr = (_vp * len(predictors))(*[P.h for P in predictors])
+    check(lib().elis_peer_attach_local(arr, len(predictors)), "elis_peer_attach_local")
 
 
 def nccl_unique_id() -> bytes:

@@ -179,6 +179,12 @@ struct elis_predictor {
   void *send = nullptr, *recv = nullptr;
   unsigned long long* mkeys = nullptr;
   int32_t* mids = nullptr;
+  // dist over peer memory (elis_peer_*): own symmetric region + every rank's as mapped here
+  uint8_t* peer_own = nullptr;
+  uint8_t* peer_map[kMaxPeers] = {};
+  bool peer_ipc[kMaxPeers] = {};   // mapped with cudaIpcOpenMemHandle (closed on destroy)
+  bool use_peer = false;
+  uint32_t peer_epoch = 0;
 
   // host-buffer iteration staging
   int32_t *d_tokens = nullptr, *d_lengths = nullptr, *d_generated = nullptr, *d_ids = nullptr, *d_count = nullptr;
@@ -266,6 +272,7 @@ const char* elis_status_string(elis_status s) {
     case ELIS_ERR_CUDA: return "CUDA error";
     case ELIS_ERR_NCCL: return "NCCL error";
     case ELIS_ERR_DEVICE_INPUT: return "device-detected input error";
+    case ELIS_ERR_PEER_TIMEOUT: return "peer-memory select: a rank never arrived";
   }
   return "unknown status";
 }
@@ -277,6 +284,8 @@ void elis_predictor_destroy(elis_predictor* p) {
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
   if (p->comm && nccl().ok) nccl().commDestroy(p->comm);
+  for (int r = 0; r < kMaxPeers; ++r)
+    if (p->peer_ipc[r]) cudaIpcCloseMemHandle(p->peer_map[r]);
   for (void* a : p->allocs) cudaFree(a);
   for (cudaEvent_t e : p->event_pool) cudaEventDestroy(e);
   delete p;
@@ -688,6 +697,7 @@ elis_status elis_dist_attach(elis_predictor* p, int32_t rank, int32_t world, con
   if (r != ncclSuccess) return fail(ELIS_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().getErrorString(r));
   p->rank = rank;
   p->world = world;
+  p->use_peer = false;  // the last attach call picks the transport
   const size_t cand = 16;  // Candidate {u64 key, i32 id, i32 pad}
   if (!p->send) {
     if (p->alloc(reinterpret_cast<uint8_t**>(&p->send), cand * kMaxBatchCap) != cudaSuccess)
@@ -700,12 +710,103 @@ elis_status elis_dist_attach(elis_predictor* p, int32_t rank, int32_t world, con
   return ELIS_OK;
 }
 
+// ---- peer-memory transport (include/elis.h)
+static elis_status peer_check(elis_predictor* p, int32_t rank, int32_t world) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(ELIS_ERR_INVALID_ARG, "rank / world (world <= 8)");
+  return ELIS_OK;
+}
+
+static elis_status peer_alloc_buffers(elis_predictor* p, int32_t rank, int32_t world) {
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!p->peer_own) {
+    if (p->alloc(&p->peer_own, peer_region_bytes()) != cudaSuccess) return fail(ELIS_ERR_OOM, "peer region");
+    CUDA_TRY(cudaDeviceSynchronize());  // the zeroed flags are in place before any peer maps it
+  }
+  if (!p->mkeys || p->world < world) {
+    if (p->alloc(&p->mkeys, static_cast<size_t>(kMaxBatchCap) * world) != cudaSuccess ||
+        p->alloc(&p->mids, static_cast<size_t>(kMaxBatchCap) * world) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "merge buffers");
+  }
+  p->rank = rank;
+  p->world = world;
+  return ELIS_OK;
+}
+
+elis_status elis_peer_export(elis_predictor* p, int32_t rank, int32_t world, void* out_handle64) {
+  elis_status s = peer_check(p, rank, world);
+  if (s != ELIS_OK) return s;
+  if (!out_handle64) return fail(ELIS_ERR_INVALID_ARG, "NULL handle");
+  s = peer_alloc_buffers(p, rank, world);
+  if (s != ELIS_OK) return s;
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p->peer_own));
+  std::memcpy(out_handle64, &h, 64);
+  return ELIS_OK;
+}
+
+elis_status elis_peer_attach(elis_predictor* p, const void* handles) {
+  if (!p || !handles) return fail(ELIS_ERR_INVALID_ARG, "NULL argument");
+  if (!p->peer_own) return fail(ELIS_ERR_INVALID_ARG, "elis_peer_export was not called");
+  CUDA_TRY(cudaSetDevice(p->device));
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (p->peer_ipc[r]) cudaIpcCloseMemHandle(p->peer_map[r]);
+    p->peer_ipc[r] = false;
+    p->peer_map[r] = nullptr;
+  }
+  for (int r = 0; r < p->world; ++r) {
+    if (r == p->rank) {
+      p->peer_map[r] = p->peer_own;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * r, 64);
+    void* m = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&m, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ELIS_ERR_CUDA, "cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
+    p->peer_map[r] = static_cast<uint8_t*>(m);
+    p->peer_ipc[r] = true;
+  }
+  p->use_peer = true;
+  p->peer_epoch = 0;
+  return ELIS_OK;
+}
+
+elis_status elis_peer_attach_local(elis_predictor* const* peers, int32_t world) {
+  if (!peers || world < 1 || world > kMaxPeers) return fail(ELIS_ERR_INVALID_ARG, "peers / world (world <= 8)");
+  for (int r = 0; r < world; ++r) {
+    if (!peers[r]) return fail(ELIS_ERR_INVALID_ARG, "NULL peer");
+    elis_status s = peer_alloc_buffers(peers[r], r, world);
+    if (s != ELIS_OK) return s;
+  }
+  for (int r = 0; r < world; ++r) {
+    elis_predictor* p = peers[r];
+    CUDA_TRY(cudaSetDevice(p->device));
+    for (int q = 0; q < world; ++q) {
+      if (peers[q]->device != p->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(peers[q]->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return fail(ELIS_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      }
+      if (p->peer_ipc[q]) cudaIpcCloseMemHandle(p->peer_map[q]);
+      p->peer_ipc[q] = false;
+      p->peer_map[q] = peers[q]->peer_own;
+    }
+    p->use_peer = true;
+    p->peer_epoch = 0;
+  }
+  return ELIS_OK;
+}
+
 elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const int32_t* generated, int32_t n_local,
                                    int32_t global_offset, int32_t batch_cap, const elis_preempt* pre,
                                    int32_t* out_ids, void* stream) {
   elis_status s = validate_select(p, pred, generated, n_local, batch_cap, pre, out_ids);
   if (s != ELIS_OK) return s;
-  if (!p->comm) return fail(ELIS_ERR_INVALID_ARG, "elis_dist_attach was not called");
+  if (!p->comm && !p->use_peer) return fail(ELIS_ERR_INVALID_ARG, "neither elis_dist_attach nor elis_peer_attach was called");
   if (global_offset < 0) return fail(ELIS_ERR_INVALID_ARG, "global_offset < 0");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(p->device));
@@ -718,6 +819,21 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
   LAUNCH(p, PC_KEYS, st,
          launch_make_keys(pred, generated, order, running, n_local, policy, allow, p->cfg.head_predicts_total,
                           static_cast<uint32_t>(global_offset), starvation_of(pre), p->sc.keys, p->sc.info, st));
+  if (p->use_peer) {
+    // 2'. peer-memory transport: local top-cap, NVLink stores + epoch flags, merge -- one kernel
+    PeerArgs pa{};
+    for (int r = 0; r < kMaxPeers; ++r) pa.region[r] = p->peer_map[r];
+    pa.rank = p->rank;
+    pa.world = p->world;
+    pa.epoch = ++p->peer_epoch;
+    if (pa.epoch == 0) pa.epoch = ++p->peer_epoch;  // never 0 (the regions' initial flag value)
+    LAUNCH(p, PC_ALLGATHER, st,
+           launch_select_dist_peer(p->sc.keys, p->sc.info, n_local, batch_cap, global_offset, pa, running, p->mkeys,
+                                   p->mids, out_ids, pre ? pre->out_count : nullptr,
+                                   pre ? pre->out_nan_count : nullptr, pre ? pre->out_preempted : nullptr,
+                                   p->sc_merge.info, p->err, st));
+    return ELIS_OK;
+  }
   LAUNCH(p, PC_SELECT, st,
          launch_select_topk(p->sc.keys, nullptr, n_local, batch_cap, p->tmp_ids, nullptr,
                             pre ? pre->out_nan_count : nullptr, p->sc, st));
@@ -796,6 +912,8 @@ elis_status elis_sync_status(elis_predictor* p) {
   p->last_err_bits = bits;
   if (bits) {
     CUDA_TRY(cudaMemset(p->err, 0, 4));
+    if (bits & ERR_PEER_TIMEOUT)
+      return fail(ELIS_ERR_PEER_TIMEOUT, "a rank's candidates never arrived (device error bits " + std::to_string(bits) + ")");
     return fail(ELIS_ERR_DEVICE_INPUT, "device error bits " + std::to_string(bits));
   }
   return ELIS_OK;

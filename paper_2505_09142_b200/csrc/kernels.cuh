@@ -10,7 +10,7 @@ namespace elis {
 enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BIAS_RESID_LN = 3 };
 
 // Device error bits (sticky; see elis.h).
-enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u };
+enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u };
 
 // ---- GEMM (gemm.cu)
 struct GemmArgs {
@@ -156,5 +156,26 @@ cudaError_t launch_assign_nodes(int32_t* load, int num_nodes, int n_new, int32_t
 cudaError_t launch_pack_candidates(const SelectScratch sc, int cap, int global_offset, void* send, cudaStream_t st);
 cudaError_t launch_unpack_candidates(const void* recv, int total, unsigned long long* keys, int32_t* ids,
                                      cudaStream_t st);
+
+// ---- multi-GPU select over peer memory (select.cu).  Every rank owns one
+// symmetric region of peer_region_bytes(): candidate keys u64 [2][kMaxPeers * kMaxBatchCap],
+// ids i32 [2][kMaxPeers * kMaxBatchCap], epoch flags u32 [2][kMaxPeers] (index = the epoch's
+// parity; rank s's candidates at s * cap).  region[r] is rank r's region as mapped here
+// (CUDA IPC, or a plain device pointer when the ranks share the process).
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+  uint8_t* region[kMaxPeers];
+  int rank, world;
+  uint32_t epoch;  // > 0, identical on every rank for the same call
+};
+size_t peer_region_bytes();
+// local top-cap -> stores into every rank's region + release flags -> acquire every rank's
+// flag of this epoch -> identical merge -> out_ids (global), out_count, merged threshold in
+// info[0..1, 4], preempt flags of this rank's n_local slots.  One launch, one CTA.
+cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32_t* local_info, int n_local, int cap,
+                                    int global_offset, PeerArgs pa, const uint8_t* running,
+                                    unsigned long long* mkeys, int32_t* mids, int32_t* out_ids, int32_t* out_count,
+                                    int32_t* out_nan, uint8_t* out_preempted, uint32_t* info, uint32_t* err,
+                                    cudaStream_t st);
 
 }  // namespace elis

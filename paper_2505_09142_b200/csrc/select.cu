@@ -69,34 +69,20 @@ __global__ void k_make_keys(const float* __restrict__ pred, const int32_t* __res
 
 constexpr int kSelThreads = 1024;
 
-// One CTA per node (per-node Priority Buffers, P:300): block w selects among the slots with
-// node[i] == w (node == NULL: one block over every slot); a node that is not ready selects
-// nothing.  Outputs of block w: out_ids[w * cap ...], out_count[w], info[8 w + {0, 1, 4, 5}].
-__global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long long* __restrict__ keys,
-                                                             const int32_t* __restrict__ ids,
-                                                             const int32_t* __restrict__ node,
-                                                             const uint8_t* __restrict__ node_ready, int n, int cap,
-                                                             int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
-                                                             int32_t* __restrict__ out_nan, uint32_t* __restrict__ info,
-                                                             unsigned long long* __restrict__ sel_keys,
-                                                             int32_t* __restrict__ sel_ids, int sort_len) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  unsigned long long* ck = reinterpret_cast<unsigned long long*>(sm);       // [sort_len]
-  int32_t* ci = reinterpret_cast<int32_t*>(ck + sort_len);                  // [sort_len]
+// Exact top-cap of one CTA (1024 threads): the cap smallest eligible keys among slots i < n
+// with mine(i) (key != UINT64_MAX and, with nodes, node[i] == w), ascending, into ck / ci
+// (sort_len entries; the tail KEY_NONE / -1).  MSB-first 8-bit radix select of the cap-th key
+// (early exit once its bucket is exactly the remaining need), compaction of the winners,
+// bitonic sort.  Returns the number selected, min(cap, eligible); *elig_out = eligible.
+__device__ int cta_topk_sorted(const unsigned long long* keys, const int32_t* ids, const int32_t* node, int w, bool ready, int n, int cap, int sort_len,
+                               unsigned long long* ck, int32_t* ci, int* elig_out) {
   __shared__ int hist[256];
   __shared__ int s_elig, s_count, s_digit, s_remaining, s_done;
   __shared__ unsigned long long s_prefix, s_mask;
-
   const int tid = threadIdx.x;
-  const int w = blockIdx.x;
-  const bool ready = !node_ready || node_ready[w];
-  out_ids += static_cast<size_t>(w) * cap;
-  if (out_count) out_count += w;
-  if (sel_keys) sel_keys += static_cast<size_t>(w) * cap;
-  if (sel_ids) sel_ids += static_cast<size_t>(w) * cap;
-  uint32_t* info_w = info + 8 * w;
   // slot i takes part in this block's selection
   auto mine = [&](int i, unsigned long long k) { return k != KEY_NONE && (!node || node[i] == w); };
+  __syncthreads();  // a previous call's readers of the shared state are done
   if (tid == 0) { s_elig = 0; s_count = 0; s_prefix = 0; s_mask = 0; s_done = 0; }
   __syncthreads();
   int e = 0;
@@ -191,6 +177,34 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
       __syncthreads();
     }
   }
+  *elig_out = s_elig;
+  return target;
+}
+
+// One CTA per node (per-node Priority Buffers, P:300): block w selects among the slots with
+// node[i] == w (node == NULL: one block over every slot); a node that is not ready selects
+// nothing.  Outputs of block w: out_ids[w * cap ...], out_count[w], info[8 w + {0, 1, 4, 5}].
+__global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long long* __restrict__ keys,
+                                                             const int32_t* __restrict__ ids,
+                                                             const int32_t* __restrict__ node,
+                                                             const uint8_t* __restrict__ node_ready, int n, int cap,
+                                                             int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
+                                                             int32_t* __restrict__ out_nan, uint32_t* __restrict__ info,
+                                                             unsigned long long* __restrict__ sel_keys,
+                                                             int32_t* __restrict__ sel_ids, int sort_len) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  unsigned long long* ck = reinterpret_cast<unsigned long long*>(sm);       // [sort_len]
+  int32_t* ci = reinterpret_cast<int32_t*>(ck + sort_len);                  // [sort_len]
+  const int tid = threadIdx.x;
+  const int w = blockIdx.x;
+  const bool ready = !node_ready || node_ready[w];
+  out_ids += static_cast<size_t>(w) * cap;
+  if (out_count) out_count += w;
+  if (sel_keys) sel_keys += static_cast<size_t>(w) * cap;
+  if (sel_ids) sel_ids += static_cast<size_t>(w) * cap;
+  uint32_t* info_w = info + 8 * w;
+  int elig = 0;
+  const int target = cta_topk_sorted(keys, ids, node, w, ready, n, cap, sort_len, ck, ci, &elig);
   for (int j = tid; j < cap; j += kSelThreads) {
     const bool v = j < target;
     out_ids[j] = v ? ci[j] : -1;
@@ -204,7 +218,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
     info_w[0] = static_cast<uint32_t>(thr);
     info_w[1] = static_cast<uint32_t>(thr >> 32);
     info_w[4] = static_cast<uint32_t>(target);
-    info_w[5] = static_cast<uint32_t>(s_elig);
+    info_w[5] = static_cast<uint32_t>(elig);
     if (out_nan && w == 0) *out_nan = static_cast<int32_t>(info[6]);
   }
 }
@@ -304,6 +318,123 @@ __global__ void k_unpack(const Candidate* __restrict__ recv, int total, unsigned
   }
 }
 
+// ---- multi-GPU select over peer memory (SURVEY.md 8e "B200-native stretch")
+//
+// The whole cross-rank exchange of Sec. 8a row a13 in one kernel: each rank's local top-cap
+// candidates are stored straight into every rank's symmetric region over NVLink / NVSwitch
+// (plain st.global through CUDA-IPC-mapped pointers), published by a release store of the call's
+// epoch into the destination's flag slot, and every rank acquires all `world` flags and runs the
+// same deterministic merge -- the NCCL all-gather, its pack / unpack kernels and two extra
+// select launches disappear.  Regions are double-buffered by epoch parity: rank s can only
+// write epoch e + 2 into a parity slot after it has seen every rank's epoch e + 1 flag, i.e.
+// after every rank finished reading epoch e from that slot.
+ELIS_DEV unsigned long long peer_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+ELIS_DEV void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+ELIS_DEV uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+constexpr size_t kPeerSlots = static_cast<size_t>(kMaxPeers) * kMaxBatchCap;   // candidates per parity
+ELIS_DEV unsigned long long* peer_keys(uint8_t* region, int par) {
+  return reinterpret_cast<unsigned long long*>(region) + par * kPeerSlots;
+}
+ELIS_DEV int32_t* peer_ids(uint8_t* region, int par) {
+  return reinterpret_cast<int32_t*>(region + 2 * kPeerSlots * 8) + par * kPeerSlots;
+}
+ELIS_DEV uint32_t* peer_flags(uint8_t* region, int par) {
+  return reinterpret_cast<uint32_t*>(region + 2 * kPeerSlots * 12) + par * kMaxPeers;
+}
+constexpr unsigned long long kPeerTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: a rank that never arrives
+
+__global__ void __launch_bounds__(kSelThreads)
+    k_select_dist_peer(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ local_info,
+                       int n_local, int cap, int global_offset, PeerArgs pa, const uint8_t* __restrict__ running,
+                       unsigned long long* mkeys, int32_t* mids, int32_t* __restrict__ out_ids,
+                       int32_t* __restrict__ out_count, int32_t* __restrict__ out_nan,
+                       uint8_t* __restrict__ out_preempted, uint32_t* __restrict__ info, uint32_t* __restrict__ err,
+                       int sort_len) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  unsigned long long* ck = reinterpret_cast<unsigned long long*>(sm);       // [sort_len]
+  int32_t* ci = reinterpret_cast<int32_t*>(ck + sort_len);                  // [sort_len]
+  __shared__ int s_timeout;
+  const int tid = threadIdx.x;
+  const int par = static_cast<int>(pa.epoch & 1u);
+  if (tid == 0) s_timeout = 0;
+  // 1. this rank's top-cap (ids = local slot index)
+  int elig = 0;
+  const int target = cta_topk_sorted(keys, nullptr, nullptr, 0, true, n_local, cap, sort_len, ck, ci, &elig);
+  // 2. push them into every rank's region (own included) at [par][rank * cap + j], global ids
+  for (int r = 0; r < pa.world; ++r) {
+    unsigned long long* pk = peer_keys(pa.region[r], par) + static_cast<size_t>(pa.rank) * cap;
+    int32_t* pi = peer_ids(pa.region[r], par) + static_cast<size_t>(pa.rank) * cap;
+    for (int j = tid; j < cap; j += kSelThreads) {
+      const bool v = j < target;
+      pk[j] = v ? ck[j] : KEY_NONE;
+      pi[j] = v ? ci[j] + global_offset : -1;
+    }
+  }
+  __syncthreads();  // every thread's peer stores precede the fence + flag store below
+  if (tid < pa.world) {
+    __threadfence_system();
+    st_release_sys_u32(peer_flags(pa.region[tid], par) + pa.rank, pa.epoch);
+  }
+  // 3. acquire every rank's flag of this epoch (bounded: a missing rank sets ERR_PEER_TIMEOUT)
+  if (tid < pa.world) {
+    const uint32_t* f = peer_flags(pa.region[pa.rank], par) + tid;
+    const unsigned long long t0 = peer_globaltimer();
+    while (static_cast<int32_t>(ld_acquire_sys_u32(f) - pa.epoch) < 0) {
+      __nanosleep(32);
+      if (peer_globaltimer() - t0 > kPeerTimeoutNs) {
+        atomicOr(err, ERR_PEER_TIMEOUT);
+        s_timeout = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const int total = pa.world * cap;
+  int got = 0;
+  if (!s_timeout) {
+    // 4. copy the world x cap candidates (written by other GPUs during this kernel) with
+    //    cache-volatile loads into local scratch, then the same merge on every rank
+    const unsigned long long* rk = peer_keys(pa.region[pa.rank], par);
+    const int32_t* ri = peer_ids(pa.region[pa.rank], par);
+    for (int j = tid; j < total; j += kSelThreads) {
+      mkeys[j] = __ldcv(rk + j);
+      mids[j] = __ldcv(ri + j);
+    }
+    __syncthreads();
+    int elig2 = 0;
+    got = cta_topk_sorted(mkeys, mids, nullptr, 0, true, total, cap, sort_len, ck, ci, &elig2);
+  }
+  // 5. outputs: global ids in priority order, count, merged threshold, this rank's preempt flags
+  for (int j = tid; j < cap; j += kSelThreads) out_ids[j] = j < got ? ci[j] : -1;
+  const unsigned long long thr = got > 0 ? ck[got - 1] : 0ull;
+  if (tid == 0) {
+    if (out_count) *out_count = got;
+    if (out_nan) *out_nan = static_cast<int32_t>(local_info[6]);
+    info[0] = static_cast<uint32_t>(thr);
+    info[1] = static_cast<uint32_t>(thr >> 32);
+    info[4] = static_cast<uint32_t>(got);
+  }
+  if (out_preempted)
+    for (int i = tid; i < n_local; i += kSelThreads) {
+      bool flag = false;
+      if (running && running[i]) {
+        const unsigned long long k = keys[i];
+        flag = !(got > 0 && k != KEY_NONE && k <= thr);
+      }
+      out_preempted[i] = flag ? 1 : 0;
+    }
+}
+
 int next_pow2(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -380,6 +511,30 @@ cudaError_t launch_pack_candidates(const SelectScratch sc, int cap, int global_o
 cudaError_t launch_unpack_candidates(const void* recv, int total, unsigned long long* keys, int32_t* ids,
                                      cudaStream_t st) {
   k_unpack<<<(total + 255) / 256, 256, 0, st>>>(static_cast<const Candidate*>(recv), total, keys, ids);
+  return cudaGetLastError();
+}
+
+size_t peer_region_bytes() { return 2 * kPeerSlots * 12 + 2 * kMaxPeers * sizeof(uint32_t); }
+
+cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32_t* local_info, int n_local, int cap,
+                                    int global_offset, PeerArgs pa, const uint8_t* running,
+                                    unsigned long long* mkeys, int32_t* mids, int32_t* out_ids, int32_t* out_count,
+                                    int32_t* out_nan, uint8_t* out_preempted, uint32_t* info, uint32_t* err,
+                                    cudaStream_t st) {
+  if (pa.world < 1 || pa.world > kMaxPeers || pa.rank < 0 || pa.rank >= pa.world || cap < 1 || cap > kMaxBatchCap)
+    return cudaErrorInvalidValue;
+  const int sort_len = next_pow2(cap < 2 ? 2 : cap);
+  const size_t smem = static_cast<size_t>(sort_len) * (sizeof(unsigned long long) + sizeof(int32_t));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_select_dist_peer, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxBatchCap * 12 + 1024));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_select_dist_peer<<<1, kSelThreads, smem, st>>>(keys, local_info, n_local, cap, global_offset, pa, running, mkeys,
+                                                   mids, out_ids, out_count, out_nan, out_preempted, info, err,
+                                                   sort_len);
   return cudaGetLastError();
 }
 
