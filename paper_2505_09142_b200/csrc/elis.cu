@@ -35,6 +35,9 @@ elis_status fail(elis_status s, const std::string& msg) {
 
 // NCCL is resolved at run time (dlopen), preferring a copy already loaded in the
 // process (torch's), so loading libelis never pins a second NCCL version.
+constexpr size_t kFcPartCap = size_t(2) << 20;  // head split-K partials (floats, 8 MB)
+constexpr int kFcCtrCap = 4096;
+
 struct NcclApi {
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
@@ -153,6 +156,8 @@ struct elis_predictor {
 
   // workspaces
   float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
+  float* fc_part = nullptr;    // head split-K partials (kFcPartCap floats) + tickets
+  uint32_t* fc_ctr = nullptr;
   // CLS-only last layer (cfg.cls_last_layer): compact per-request rows [max_requests, *]
   float* hres_c = nullptr;
   uint16_t *ctx_c = nullptr, *hb_c = nullptr, *g_c = nullptr;
@@ -449,6 +454,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   ALLOC(p->pooled, static_cast<size_t>(N) * H);
   ALLOC(p->z0, static_cast<size_t>(N) * cfg->head_hidden);
   ALLOC(p->z1, static_cast<size_t>(N) * cfg->head_hidden);
+  ALLOC(p->fc_part, kFcPartCap);
+  ALLOC(p->fc_ctr, kFcCtrCap);
   p->key_cap = std::max(N, 65536);
   ALLOC(p->sc.keys, p->key_cap);
   ALLOC(p->sc.info, 8 * kMaxNodes);
@@ -573,7 +580,9 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   const int nl = c.head_layers;
   for (int j = 0; j < nl - 1; ++j) {
     float* y = bufs[j & 1];
-    LAUNCH(p, PC_HEAD_FC, st, launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, st));
+    const FcWork wk{p->fc_part, kFcPartCap, p->fc_ctr, kFcCtrCap, p->num_sms};
+    LAUNCH(p, PC_HEAD_FC, st,
+           launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st));
     x = y;
   }
   LAUNCH(p, PC_HEAD_OUT, st,
@@ -1081,7 +1090,19 @@ elis_status elis_op_layernorm(const float* u, const float* gamma, const float* b
 elis_status elis_op_fc_f32(const float* X, const float* W, const float* b, float* Y, int32_t n, int32_t N, int32_t K,
                            int32_t relu, void* stream) {
   if (!X || !W || !b || !Y || n < 0 || N < 1 || K < 1) return fail(ELIS_ERR_INVALID_ARG, "fc arguments");
-  CUDA_TRY(launch_fc_f32(X, W, b, Y, n, N, K, relu, static_cast<cudaStream_t>(stream)));
+  // test entry: one process-wide split-K workspace (op calls are serialised by the caller)
+  static float* part = nullptr;
+  static uint32_t* ctr = nullptr;
+  if (!part) {
+    CUDA_TRY(cudaMalloc(&part, kFcPartCap * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&ctr, kFcCtrCap * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(ctr, 0, kFcCtrCap * sizeof(uint32_t)));
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const FcWork wk{part, kFcPartCap, ctr, kFcCtrCap, sms};
+  CUDA_TRY(launch_fc_f32(X, W, b, Y, n, N, K, relu, wk, static_cast<cudaStream_t>(stream)));
   return ELIS_OK;
 }
 

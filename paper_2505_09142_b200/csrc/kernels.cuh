@@ -113,8 +113,17 @@ cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens,
 cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, float* dst, cudaStream_t st);
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
                         float* pooled, cudaStream_t st);
+// split-K workspace of the exact-fp32 head (part == nullptr: no split)
+struct FcWork {
+  float* part;        // [S][n][N] partial tiles
+  size_t part_cap;    // floats
+  uint32_t* ctr;      // [tiles] arrival tickets, zero between launches
+  int ctr_cap;
+  int num_sms;
+};
+int fc_splits(int n, int N, int K, int num_sms, size_t part_cap, int ctr_cap);
 cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,
-                          cudaStream_t st);
+                          const FcWork& wk, cudaStream_t st);
 cudaError_t launch_head_out(const float* Z, const float* w, const float* b, int n, int K, float* out_pred,
                             const int32_t* out_slot, cudaStream_t st);
 

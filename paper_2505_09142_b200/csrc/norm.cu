@@ -186,11 +186,19 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
   const int lane = lane_id();
   const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp_id();
   if (t >= T) return;
-  // request containing token t: largest i with cu[i] <= t (binary search over n+1 offsets)
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (static_cast<long long>(__ldg(cu + mid)) <= t) lo = mid; else hi = mid - 1;
+  // request containing token t: largest i with cu[i] <= t.  32-way search by the whole warp
+  // (each lane probes one offset, a ballot picks the segment): 2 dependent loads for n <= 1024
+  // instead of log2(n) for a binary search.  Invariant: cu[lo] <= t, answer in [lo, lo + len).
+  int lo = 0, len = n;
+  while (len > 1) {
+    const int step = (len + 31) >> 5;
+    const int idx = lo + lane * step;
+    const bool ok = idx < lo + len && static_cast<long long>(__ldg(cu + idx)) <= t;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    const int k = 31 - __clz(bal);  // lane 0 always passes (cu[lo] <= t)
+    const int nlo = lo + k * step;
+    len = min(step, lo + len - nlo);
+    lo = nlo;
   }
   int p = static_cast<int>(t - __ldg(cu + lo));
   p = min(max(p, 0), max_position - 1);

@@ -144,6 +144,12 @@ def test_fc_f32_parity(cuda_lib, n, N, K):
         if relu:
             ref = np.maximum(ref, 0)
         np.testing.assert_allclose(to_np(Y), ref, rtol=2e-5, atol=2e-5)
+        # split-K (these shapes take 1-8 splits): the tickets reset, so a repeat is bit-identical
+        Y2 = torch.empty(n, N, device="cuda")
+        binding.op_fc_f32(torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), Y2,
+                          relu)
+        torch.cuda.synchronize()
+        assert torch.equal(Y, Y2)
 
 
 @pytest.mark.parametrize("M,N,K", [(300, 768, 768), (1000, 768, 3072), (129, 1024, 1024), (129, 1024, 4096),
