@@ -53,6 +53,10 @@ def parse():
                          "f4(iii) -- the precision that meets the north_star parity bars on every tested "
                          "input at bf16's speed, DESIGN.md R21), bf16 (default for the tiny d=32 encoder), or "
                          "fp8 E4M3 GEMMs (row f4(i); looser tolerance, DESIGN.md R20)")
+    ap.add_argument("--residual", choices=["fp32", "fp16"], default=None,
+                    help="residual stream between layers: the fp16 copy the GEMMs already read (default with fp16 "
+                         "operands: elis_config.residual16, meets the north_star bars on every tested input, "
+                         "DESIGN.md R23) or fp32 (default otherwise, DESIGN.md R12)")
     ap.add_argument("--pooling", choices=["mean", "cls"], default="mean",
                     help="mean (P:359, default) or CLS (P:138) pooling (DESIGN.md R2)")
     ap.add_argument("--cls-last-layer", action="store_true",
@@ -113,6 +117,7 @@ def config_desc(args, T_local, world):
         "batch_cap": args.cap,
         "pooling": args.pooling + (" (last layer on CLS rows only)" if args.cls_last_layer else ""),
         "precision": args.precision,
+        "residual": args.residual,
         "parallelism": f"request-sharded dp{world}" if world > 1 else "single GPU",
         **({"transport": args.transport_used} if world > 1 else {}),
         "l2": "no flush: per-step working set (218 MB bf16 weights + >=0.5 GB activations) exceeds the 126 MB L2",
@@ -353,6 +358,7 @@ def run_elis(args):
         tokens = windows[0][4]
         gen = gen_t[:n]
         P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision,
+                              residual16=args.residual == "fp16",
                               cls_last_layer=args.cls_last_layer)
         d_table = torch.zeros(F, device="cuda")
         d_gen = torch.from_numpy(gen_t).cuda()
@@ -373,6 +379,7 @@ def run_elis(args):
         n, T = len(L), int(L.sum())
         T_roof = T
         P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, n, device=local, precision=args.precision,
+                              residual16=args.residual == "fp16",
                               cls_last_layer=args.cls_last_layer)
         d_tok = torch.from_numpy(tokens).cuda()
         d_len = torch.from_numpy(L).cuda()
@@ -527,6 +534,10 @@ def main():
         raise SystemExit("--cls-last-layer needs --pooling cls")
     if args.precision is None:
         args.precision = "fp16" if inputs.CONFIGS[args.config].head_dim == 64 else "bf16"
+    if args.residual is None:
+        args.residual = "fp16" if args.precision == "fp16" and not args.cls_last_layer else "fp32"
+    if args.residual == "fp16" and (args.precision != "fp16" or args.cls_last_layer):
+        raise SystemExit("--residual fp16 needs --precision fp16 and no --cls-last-layer")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define ELIS_ABI_VERSION 3
+#define ELIS_ABI_VERSION 4
 
 typedef enum {
   ELIS_OK = 0,
@@ -90,6 +90,12 @@ typedef struct {
   int32_t cls_last_layer;     /* 1 with pooling = CLS: the last layer computes only each      */
                               /* request's CLS row (exact: nothing else reaches the head;     */
                               /* SURVEY.md Sec. 8f row f4(ii)); needs head dim 64             */
+  int32_t residual16;         /* 1 with precision = FP16: the residual stream between layers  */
+                              /* is the fp16 copy the GEMMs already read (SURVEY.md Sec. 8b    */
+                              /* `residual_fp32 = 0`): the LayerNorm GEMM epilogues read and   */
+                              /* write 2 bytes per element instead of 4 + 2 (+4) and no fp32   */
+                              /* stream exists; LN statistics stay fp32.  0 (default): fp32    */
+                              /* residual stream (R12).  Not with cls_last_layer.    */
 } elis_config;
 
 typedef struct elis_predictor elis_predictor;

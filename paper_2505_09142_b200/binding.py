@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 
 ELIS_OK = 0
-ABI_VERSION = 3  # include/elis.h ELIS_ABI_VERSION
+ABI_VERSION = 4  # include/elis.h ELIS_ABI_VERSION
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
           6: "nccl", 7: "device input", 8: "peer timeout"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
@@ -35,7 +35,7 @@ class ElisConfig(ctypes.Structure):
                 ("num_layers", _i32), ("hidden", _i32), ("num_heads", _i32), ("intermediate", _i32),
                 ("ln_eps", _f32), ("pooling", _i32), ("head_layers", _i32), ("head_hidden", _i32),
                 ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32),
-                ("precision", _i32), ("cls_last_layer", _i32)]
+                ("precision", _i32), ("cls_last_layer", _i32), ("residual16", _i32)]
 
 
 class ElisStarvation(ctypes.Structure):
@@ -143,11 +143,12 @@ def _stream(stream):
 
 
 def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
-                head_predicts_total: bool = False, precision: str = "bf16", cls_last_layer: bool = False) -> ElisConfig:
+                head_predicts_total: bool = False, precision: str = "bf16", cls_last_layer: bool = False,
+                residual16: bool = False) -> ElisConfig:
     return ElisConfig(ABI_VERSION, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
                       cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
                       int(head_predicts_total), int(max_tokens), int(max_requests), int(device), PRECISION[precision],
-                      int(cls_last_layer))
+                      int(cls_last_layer), int(residual16))
 
 
 class Predictor:
@@ -155,11 +156,13 @@ class Predictor:
 
     def __init__(self, cfg: inputs.EncoderConfig, flat_weights: np.ndarray, max_tokens: int, max_requests: int,
                  device: int = 0, head_predicts_total: bool = False, precision: str = "bf16",
-                 cls_last_layer: bool = False):
+                 cls_last_layer: bool = False, residual16: bool = False):
         L = lib()
         self.cfg = cfg
         self.precision = precision
-        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total, precision, cls_last_layer)
+        self.residual16 = residual16
+        self.c = make_config(cfg, max_tokens, max_requests, device, head_predicts_total, precision, cls_last_layer,
+                             residual16)
         flat = np.ascontiguousarray(flat_weights, dtype=np.float32)
         need = L.elis_weight_count(ctypes.byref(self.c))
         if need != flat.size:

@@ -100,6 +100,9 @@ bool config_valid(const elis_config* c, std::string* why) {
   if (c->precision != ELIS_PREC_BF16 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
     return bad("FP8 / FP16 need head dim 64 and hidden, intermediate multiples of 256");
   if (c->cls_last_layer != 0 && c->cls_last_layer != 1) return bad("cls_last_layer must be 0 or 1");
+  if (c->residual16 != 0 && c->residual16 != 1) return bad("residual16 must be 0 or 1");
+  if (c->residual16 && (c->precision != ELIS_PREC_FP16 || c->cls_last_layer))
+    return bad("residual16 needs precision = FP16 and cls_last_layer = 0");
   if (c->cls_last_layer && (c->pooling != ELIS_POOL_CLS || d != 64))
     return bad("cls_last_layer needs pooling = CLS and head dim 64");
   return true;
@@ -429,7 +432,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   p->head_dims.push_back(1);
 
   // ---- workspaces
-  ALLOC(p->h32, static_cast<size_t>(T) * H);
+  if (!cfg->residual16) ALLOC(p->h32, static_cast<size_t>(T) * H);  // residual16: the stream is hb
   ALLOC(p->hb, static_cast<size_t>(T) * H);
   ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
   ALLOC(p->ctx, static_cast<size_t>(T) * H);
@@ -484,6 +487,13 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
                              kF8ScaleGelu) &&
            make_gemm_plan_f8(&L.p_ffn2, p->g, T, L.w2, L.s2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN,
                              kF8ScaleHidden);
+    else if (cfg->residual16)  // the LN epilogues read the residual from, and write LN(.) into, hb
+      ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
+           make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, reinterpret_cast<const float*>(p->hb), p->hb, 0, H, H,
+                          EPI_BIAS_RESID16_LN) &&
+           make_gemm_plan(&L.p_ffn1, p->hb, T, L.w1, L.b1, nullptr, p->g, 0, F, H, EPI_BIAS_GELU_BF16) &&
+           make_gemm_plan(&L.p_ffn2, p->g, T, L.w2, L.b2, reinterpret_cast<const float*>(p->hb), p->hb, 0, H, F,
+                          EPI_BIAS_RESID16_LN);
     else
       ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
            make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, p->h32, p->h32, 0, H, H, EPI_BIAS_RESID_LN) &&
@@ -574,7 +584,9 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   if (c.cls_last_layer)  // row i of the compact buffer is request i's CLS row
     LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st));
   else
-    LAUNCH(p, PC_POOL, st, launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
+    LAUNCH(p, PC_POOL, st,
+           c.residual16 ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st)
+                        : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
   const float* x = p->pooled;
   float* bufs[2] = {p->z0, p->z1};
   const int nl = c.head_layers;
@@ -934,7 +946,10 @@ elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* 
   if (!p || !dst) return fail(ELIS_ERR_INVALID_ARG, "NULL argument");
   const int64_t need = p->last_T * p->cfg.hidden;
   if (count < need) return fail(ELIS_ERR_INVALID_ARG, "dst too small");
-  CUDA_TRY(cudaMemcpyAsync(dst, p->h32, need * 4, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  if (p->cfg.residual16)  // the final hidden states are the fp16 stream
+    CUDA_TRY(launch_f16_to_f32(p->hb, dst, need, static_cast<cudaStream_t>(stream)));
+  else
+    CUDA_TRY(cudaMemcpyAsync(dst, p->h32, need * 4, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
   if (p->cfg.cls_last_layer)  // the final CLS rows live in the compact buffer
     CUDA_TRY(launch_scatter_rows(p->hres_c, p->cu, p->last_n, p->cfg.hidden, dst, static_cast<cudaStream_t>(stream)));
   return ELIS_OK;

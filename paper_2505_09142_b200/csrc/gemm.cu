@@ -81,16 +81,18 @@ struct GemmCfg {
 // been read): the freed 64 KB buy a fourth and a fifth operand stage.
 template <int BN, int EPI, bool DEEP, int PREC>
 struct SmemPlan {
-  static constexpr bool LN = EPI == EPI_BIAS_RESID_LN;
+  static constexpr bool LN16 = EPI == EPI_BIAS_RESID16_LN;  // 16-bit residual stream, no fp32 output
+  static constexpr bool LN = EPI == EPI_BIAS_RESID_LN || LN16;
   static constexpr bool RES = LN || EPI == EPI_BIAS_RESID_F32;
-  static constexpr bool OUT_F32 = RES;                 // f32 staging (4 KB per warp)
+  static constexpr bool OUT_F32 = RES && !LN16;        // f32 staging (4 KB per warp)
   static constexpr bool OUT_BF16 = LN || !RES;         // bf16 staging (2 KB per warp)
   static constexpr int EW = epi_warps<EPI, PREC>();
   static constexpr int NSTG = (RES || EW == 16) ? 1 : 2;  // staging buffers per warp
   static constexpr int NRES = (RES && DEEP) ? 1 : 2;   // residual slots per warp
-  static constexpr bool F32_IN_RES = LN && DEEP;        // fp32 output staged in the residual slot
-  static constexpr int STAGES = RES ? (DEEP ? (F32_IN_RES ? 5 : 4) : 3) : 5;
-  static constexpr int RES_SLOT = kBox * kBox * 4;     // 4 KB fp32 residual box
+  static constexpr bool F32_IN_RES = LN && DEEP && !LN16;  // fp32 output staged in the residual slot
+  // LN16 halves the residual slots and drops the fp32 staging: 5 operand stages either way
+  static constexpr int STAGES = RES ? ((DEEP || LN16) ? (F32_IN_RES || LN16 ? 5 : 4) : 3) : 5;
+  static constexpr int RES_SLOT = kBox * kBox * (LN16 ? 2 : 4);  // 4 KB fp32 / 2 KB fp16 residual box
   static constexpr int RES_BYTES = RES ? EW * NRES * RES_SLOT : 0;
   static constexpr int STG_F32 = kBox * kBox * 4;      // 4 KB
   static constexpr int STG_BF16 = kBox * kBox * 2;     // 2 KB
@@ -423,10 +425,24 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
           mbar_wait(&rbar[s], (rpar >> s) & 1u);
           rpar ^= 1u << s;
           const uint8_t* src = rslot + s * SP::RES_SLOT;
+          if constexpr (SP::LN16) {  // 32 fp16 of this row: four 16-byte pieces, SWIZZLE_64B
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float4 rr = *reinterpret_cast<const float4*>(src + sw128_off(lane, k));
-            v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
+            for (int k = 0; k < 4; ++k) {
+              const uint4 rr = *reinterpret_cast<const uint4*>(src + sw64_off(lane, k));
+              const uint32_t w4[4] = {rr.x, rr.y, rr.z, rr.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[e]));
+                v[8 * k + 2 * e] += f.x;
+                v[8 * k + 2 * e + 1] += f.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float4 rr = *reinterpret_cast<const float4*>(src + sw128_off(lane, k));
+              v[4 * k] += rr.x; v[4 * k + 1] += rr.y; v[4 * k + 2] += rr.z; v[4 * k + 3] += rr.w;
+            }
           }
           __syncwarp();  // every lane has read slot s
           if (c + NRES < CH) load_res(row0, col0 + NRES * 32, c + NRES);
@@ -532,11 +548,13 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
           }
           uint8_t* b = next_stage();   // NSTG = 1: every earlier store (incl. from the slot) has read
           uint8_t* b32 = SP::F32_IN_RES ? rslot : b;
+          if constexpr (SP::OUT_F32) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            *reinterpret_cast<float4*>(b32 + sw128_off(lane, k)) =
-                make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
-          uint8_t* bb = SP::F32_IN_RES ? b : b + SP::STG_F32;
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(b32 + sw128_off(lane, k)) =
+                  make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+          }
+          uint8_t* bb = (SP::F32_IN_RES || !SP::OUT_F32) ? b : b + SP::STG_F32;
           if constexpr (F8) {
             stage_e4m3_row(bb, lane, y, args.out_scale);
           } else {
@@ -581,7 +599,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
   const int num_n = g.args.N / BN;
-  const bool ln = EPI == EPI_BIAS_RESID_LN;
+  const bool ln = EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID16_LN;
   const int cpairs = ln ? num_n : 1;
   const int csize = 2 * cpairs;
   if (cpairs > kMaxCluster) return cudaErrorInvalidValue;
@@ -639,6 +657,9 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
   if (g.f16) {  // fp16 operands and 16-bit outputs
     if (!b256) return cudaErrorInvalidValue;
     switch (g.epi) {
+      case EPI_BIAS_RESID16_LN:
+        return deep ? launch_bn<256, EPI_BIAS_RESID16_LN, true, 2>(g, num_sms, st)
+                    : launch_bn<256, EPI_BIAS_RESID16_LN, false, 2>(g, num_sms, st);
       case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, 2>(g, num_sms, st);
       case EPI_BIAS_GELU_BF16: return launch_bn<256, EPI_BIAS_GELU_BF16, false, 2>(g, num_sms, st);
       case EPI_BIAS_RESID_LN:
@@ -711,7 +732,7 @@ bool make_tmap_bf16_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
 bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
                     const float* resid, void* out, int M, int N, int K, int epi) {
   if (N % 128 != 0 || K % BK != 0 || M < 0) return false;
-  if (epi == EPI_BIAS_RESID_LN && N / gemm_block_n(N) > kMaxCluster) return false;
+  if ((epi == EPI_BIAS_RESID_LN || epi == EPI_BIAS_RESID16_LN) && N / gemm_block_n(N) > kMaxCluster) return false;
   g->epi = epi;
   g->f8 = 0;
   g->f16 = 0;
@@ -726,7 +747,15 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
   if (!make_tmap_bf16_kmajor(&g->tmB, W, N, K, gemm_block_n(N) / 2)) return false;
   const bool res = epi == EPI_BIAS_RESID_F32 || epi == EPI_BIAS_RESID_LN;
   // epilogue boxes: fp32 32 x 32 (128 B rows, SWIZZLE_128B); bf16 32 x 32 (64 B rows, SWIZZLE_64B)
-  if (res) {
+  if (epi == EPI_BIAS_RESID16_LN) {  // residual in and normalised rows out: the same 16-bit buffer
+    if (!resid || !make_tmap_2d(&g->tmR, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, resid, a_rows, N, kBox, kBox,
+                                CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
+    if (!make_tmap_2d(&g->tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, a_rows, N, kBox, kBox,
+                      CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
+    g->tmOb = g->tmO;
+  } else if (res) {
     if (!resid || !make_tmap_2d(&g->tmR, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, resid, a_rows, N, kBox, kBox,
                                 CU_TENSOR_MAP_SWIZZLE_128B))
       return false;

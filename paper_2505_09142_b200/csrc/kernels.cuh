@@ -7,7 +7,10 @@
 
 namespace elis {
 
-enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BIAS_RESID_LN = 3 };
+// EPI_BIAS_RESID16_LN: as RESID_LN with the residual stream held in 16 bits (fp16): the residual
+// is read from, and the normalised row written to, the same fp16 [M, N] buffer (no fp32 copy)
+enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BIAS_RESID_LN = 3,
+       EPI_BIAS_RESID16_LN = 4 };
 
 // Device error bits (sticky; see elis.h).
 enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u };
@@ -113,6 +116,10 @@ cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens,
 cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, float* dst, cudaStream_t st);
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
                         float* pooled, cudaStream_t st);
+// mean / CLS pooling over the fp16 residual stream (elis_config.residual16)
+cudaError_t launch_pool16(const uint16_t* h16, const int32_t* cu_seqlens, int n, int H, int pooling,
+                          const uint32_t* err, float* pooled, cudaStream_t st);
+cudaError_t launch_f16_to_f32(const uint16_t* src, float* dst, int64_t count, cudaStream_t st);
 // split-K workspace of the exact-fp32 head (part == nullptr: no split)
 struct FcWork {
   float* part;        // [S][n][N] partial tiles

@@ -132,9 +132,11 @@ __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamm
 #pragma unroll
     for (int c = 0; c < RL::C; ++c) y[c] = (x[j * RL::C + c] - mean) * rstd * __ldg(gamma + base + c) + __ldg(beta + base + c);
     if constexpr (RL::C == 8) {
-      float4* o = reinterpret_cast<float4*>(out32 + base);
-      o[0] = make_float4(y[0], y[1], y[2], y[3]);
-      o[1] = make_float4(y[4], y[5], y[6], y[7]);
+      if (out32) {  // NULL: no fp32 residual stream (elis_config.residual16)
+        float4* o = reinterpret_cast<float4*>(out32 + base);
+        o[0] = make_float4(y[0], y[1], y[2], y[3]);
+        o[1] = make_float4(y[4], y[5], y[6], y[7]);
+      }
       if (outb && f8_scale > 0.f)  // E4M3 bytes (FP8 GEMM operand, R20)
         *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(outb) + base) =
             make_uint2(pack_e4m3x4(y[0] * f8_scale, y[1] * f8_scale, y[2] * f8_scale, y[3] * f8_scale),
@@ -147,7 +149,7 @@ __device__ void ln_finish_row(float (&x)[H / 32], const float* __restrict__ gamm
             make_uint4(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]), pack_bf16x2(y[4], y[5]), pack_bf16x2(y[6], y[7]));
     } else {
       static_assert(RL::C == 4, "row chunk");
-      *reinterpret_cast<float4*>(out32 + base) = make_float4(y[0], y[1], y[2], y[3]);
+      if (out32) *reinterpret_cast<float4*>(out32 + base) = make_float4(y[0], y[1], y[2], y[3]);
       if (outb) *reinterpret_cast<uint2*>(outb + base) = make_uint2(pack_bf16x2(y[0], y[1]), pack_bf16x2(y[2], y[3]));
     }
   }
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
   uint16_t* hrow = nullptr;
   if (hb) hrow = f8_scale > 0.f ? reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(hb) + static_cast<size_t>(t) * H)
                                 : hb + static_cast<size_t>(t) * H;
-  ln_finish_row<H>(x, gamma, beta, eps, h32 + static_cast<size_t>(t) * H, hrow, lane, f8_scale, f16);
+  ln_finish_row<H>(x, gamma, beta, eps, h32 ? h32 + static_cast<size_t>(t) * H : nullptr, hrow, lane, f8_scale, f16);
 }
 
 template <int H>

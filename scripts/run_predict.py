@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8", "fp16"])
     ap.add_argument("--pooling", default="mean", choices=["mean", "cls"])
     ap.add_argument("--cls-last-layer", action="store_true", help="CLS pooling: last layer on CLS rows only")
+    ap.add_argument("--residual16", action="store_true", help="fp16 residual stream (with --precision fp16)")
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
     if a.pooling == "cls":
@@ -42,7 +43,7 @@ def main():
     tok = inputs.make_tokens(L, seed=0)
     T = int(L.sum())
     p = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg)), max_tokens=T, max_requests=a.n,
-                         precision=a.precision, cls_last_layer=a.cls_last_layer)
+                         precision=a.precision, cls_last_layer=a.cls_last_layer, residual16=a.residual16)
     dev = torch.device("cuda:0")
     t_tok = torch.from_numpy(tok).to(dev)
     t_len = torch.from_numpy(L.astype(np.int32)).to(dev)

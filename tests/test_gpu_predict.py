@@ -19,7 +19,10 @@ CLS_PRED_RTOL = 3e-2
 
 
 def make_predictor(name, max_tokens, max_requests, pooling=inputs.POOL_MEAN, **kw):
+    """precision "fp16-r16": fp16 operands with the fp16 residual stream (elis_config.residual16)."""
     from paper_2505_09142_b200 import binding
+    if kw.get("precision") == "fp16-r16":
+        kw = {**kw, "precision": "fp16", "residual16": True}
     cfg = inputs.EncoderConfig(**{**inputs.CONFIGS[name].to_dict(), "pooling": pooling})
     W = inputs.make_weights(cfg, seed=0)
     flat = inputs.flatten_weights(cfg, W)
@@ -83,7 +86,7 @@ def test_cfg1_tiny_full_parity_and_select(cuda_lib, pooling):
     P.close()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp16-r16"])
 def test_base_ragged_parity(cuda_lib, precision):
     """BGE-base, ragged lengths spanning several GEMM/attention tiles and ragged tails."""
     from oracle import head as ohead
@@ -100,7 +103,7 @@ def test_base_ragged_parity(cuda_lib, precision):
     P.close()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp8"])
+@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp16-r16", "fp8"])
 def test_batch_invariance_bitwise(cuda_lib, precision):
     """pred_i is bitwise identical whether request i is encoded alone, in a batch, or in a
     different batch order (row-independent GEMMs, per-request attention/pool/head)."""
@@ -172,7 +175,7 @@ def test_iteration_host_matches_device_path(cuda_lib):
     P.close()
 
 
-@pytest.mark.parametrize("precision,k", [("bf16", 6), ("fp16", 16)])
+@pytest.mark.parametrize("precision,k", [("bf16", 6), ("fp16", 16), ("fp16-r16", 16)])
 def test_cfg2_full_size_sampled_parity(cuda_lib, precision, k):
     """BASELINE.json configs[1] at full size in the bench's launch configuration
     (BGE-base, 256 trace-shaped requests): sampled predictions vs the oracle, and the
@@ -199,7 +202,7 @@ def test_cfg2_full_size_sampled_parity(cuda_lib, precision, k):
     P.close()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp16"])
+@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp16-r16"])
 def test_cfg3_large_4096_ragged_sampled_parity(cuda_lib, precision):
     """BASELINE.json configs[2]: BGE-large re-predicting 4,096 ragged requests of 32-512
     tokens (uniform lengths, T ~ 1.1M) in one call; stratified sample vs the oracle, the

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert binding.lib().elis_abi_version() == binding.ABI_VERSION == 3
+    assert binding.lib().elis_abi_version() == binding.ABI_VERSION == 4
 
 
 @pytest.mark.parametrize("name", ["tiny", "base", "large"])
