@@ -215,13 +215,22 @@ def kernel_roofline(prof: dict, cfg, T: int, L: np.ndarray, peaks: dict, traffic
         "gemm_ffn2": 2.0 * Tr * F * H,
         "attention": attn,
     }
+    # exact-fp32 head FC (FFMA on CUDA cores): FLOPs per launch averaged over its 7 launches; peak =
+    # 148 SMs x 128 FP32 lanes x 2 FLOP x max SM clock
+    hd = [H] + [1024] * 6
+    fc_flops = 2.0 * len(L) * sum(k * 1024 for k in hd) / len(hd)
     bytes_ = {  # algorithmic HBM bytes per launch
         "layernorm": 10.0 * T * H,          # read u f32, write h f32 + h bf16
         "embed_ln": T * (4 + 2 * H + 10.0 * H),
     }
     name, (ms, cnt) = max(prof.items(), key=lambda kv: kv[1][0])
     avg_s = ms / cnt / 1e3
-    if name in flops:
+    if name == "head_fc":
+        bound, unit = "alu", "TFLOP/s"
+        achieved = fc_flops / avg_s / 1e12
+        peak = round(148 * 128 * 2 * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12, 1)
+        peak_src = "derived: 148 SMs x 128 FP32 FMA lanes x 2 x max SM clock (MEASURED_PEAKS.json sm_max_mhz)"
+    elif name in flops:
         bound, unit = "tensor", "TFLOP/s"
         achieved = flops[name] / avg_s / 1e12
         peak = peaks.get("bf16_tflops_sustained") or 1400.0
