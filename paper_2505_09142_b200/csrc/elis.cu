@@ -1061,6 +1061,25 @@ elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* b
   return ELIS_OK;
 }
 
+elis_status elis_op_gemm_ln16(const uint16_t* A, const uint16_t* W, const float* bias, uint16_t* resid_inout,
+                              const float* gamma, const float* beta, float eps, int32_t M, int32_t N, int32_t K,
+                              void* stream) {
+  if (!A || !W || !bias || !resid_inout || !gamma || !beta || M < 1 || N < 256 || N % 256 || K < 64 || K % 64 ||
+      N / 256 > 4)
+    return fail(ELIS_ERR_INVALID_ARG, "gemm_ln16 arguments");
+  GemmPlan g;
+  if (!make_gemm_plan(&g, A, M, W, bias, reinterpret_cast<const float*>(resid_inout), resid_inout, M, N, K,
+                      EPI_BIAS_RESID16_LN) ||
+      !gemm_plan_set_ln(&g, resid_inout, gamma, beta, eps, static_cast<uint64_t>(M)))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  g.f16 = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
 elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T, int32_t hidden,
                               int32_t num_heads, uint16_t* ctx, void* stream) {
   if (!qkv || !lengths || !ctx || n < 1 || T < n || num_heads < 1 || hidden % num_heads)

@@ -52,6 +52,18 @@ def main():
                                                       torch.ones(H, device=dev), torch.zeros(H, device=dev), 1e-12,
                                                       torch.empty(M, H, dtype=torch.bfloat16, device=dev)),
     }
+    if "--r16" in sys.argv:  # fp16 operands, fp16 residual stream (EPI_BIAS_RESID16_LN)
+        hh, gh = hb.half(), gg.half()
+        shapes = {
+            "qkv fp16": lambda: binding.op_gemm(hh, rnd(3 * H, H).half(), rnd(3 * H).float(),
+                                                torch.empty(M, 3 * H, dtype=torch.half, device=dev), 0),
+            "out+LN16 (K=768)": lambda: binding.op_gemm_ln16(hh, rnd(H, H).half(), rnd(H).float(), rnd(M, H).half(),
+                                                            torch.ones(H, device=dev), torch.zeros(H, device=dev),
+                                                            1e-12),
+            "ffn2+LN16 (K=3072)": lambda: binding.op_gemm_ln16(gh, rnd(H, F).half(), rnd(H).float(), rnd(M, H).half(),
+                                                              torch.ones(H, device=dev), torch.zeros(H, device=dev),
+                                                              1e-12),
+        }
     if "--fp8" in sys.argv:  # E4M3 operands (kind::f8f6f4) on the same shapes
         def f8(*shape, scale=4.0):
             return (torch.randn(*shape, generator=g) * scale).to(torch.float8_e4m3fn).view(torch.uint8).to(dev)

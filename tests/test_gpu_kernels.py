@@ -174,3 +174,28 @@ def test_gemm_fused_residual_layernorm_parity(cuda_lib, M, N, K):
     ref = oenc.layer_norm(oenc.linear(A64, W64, b) + res, g, be, 1e-12)
     np.testing.assert_allclose(to_np(h), ref, rtol=0, atol=2e-4)
     np.testing.assert_allclose(to_np(hb), ref, rtol=8e-3, atol=1e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 768, 768), (1000, 768, 3072), (129, 1024, 1024), (77, 256, 128),
+                                   (1, 768, 768), (5000, 768, 768)])
+def test_gemm_fused_residual16_layernorm_parity(cuda_lib, M, N, K):
+    """The fp16-residual LayerNorm epilogue (EPI_BIAS_RESID16_LN, elis_config.residual16):
+    fp16 A / W / residual, fp32 v and statistics, fp16 LN output written in place over the
+    residual -- vs the oracle on the same fp16-representable inputs, to one fp16 rounding."""
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(M + N + K + 1)
+    A = torch.from_numpy(rng.normal(0, 1, (M, K))).half()
+    W = torch.from_numpy(rng.normal(0, 0.03, (N, K))).half()
+    res = torch.from_numpy(rng.normal(0.2, 1.5, (M, N))).half()
+    b = rng.normal(0, 0.1, N).astype(np.float32)
+    g = (1 + rng.uniform(-0.1, 0.1, N)).astype(np.float32)
+    be = rng.normal(0, 0.02, N).astype(np.float32)
+    h = res.cuda()
+    binding.op_gemm_ln16(A.cuda(), W.cuda(), torch.from_numpy(b).cuda(), h, torch.from_numpy(g).cuda(),
+                         torch.from_numpy(be).cuda(), 1e-12)
+    torch.cuda.synchronize()
+    ref = oenc.layer_norm(oenc.linear(A.double().numpy(), W.double().numpy(), b) + res.double().numpy(), g, be, 1e-12)
+    got = h.float().cpu().numpy().astype(np.float64)
+    # one fp16 rounding of |y| <= ~6 (2^-9 relative) plus the fp32 accumulation
+    np.testing.assert_allclose(got, ref, rtol=1.5e-3, atol=2e-4)
