@@ -223,14 +223,16 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
  * CUDA-IPC-mapped pointers and published by an epoch flag (st.release.sys); each rank then
  * acquires all `world` flags and runs the identical merge.  Results are bit-identical to the
  * NCCL transport.  Setup, once per predictor:
- *   1. elis_peer_export(p, rank, world, handle): allocates this rank's region (~0.8 MB) and
- *      writes its 64-byte cudaIpcMemHandle_t to `handle` (HOST memory);
+ *   1. elis_peer_export(p, rank, world, handle): allocates (once) and clears this rank's region
+ *      (~0.8 MB) and writes its 64-byte cudaIpcMemHandle_t to `handle` (HOST memory);
  *   2. the caller all-gathers the handles in rank order (e.g. torch.distributed);
  *   3. elis_peer_attach(p, handles): maps every other rank's region (HOST array world x 64 B).
  * From then on elis_isrtf_select_dist uses this transport.  Every rank must make the same
  * sequence of elis_isrtf_select_dist calls (like a collective); world <= 8.  A rank that never
  * arrives makes the waiting ranks give up after 10 s with the sticky ELIS_ERR_PEER_TIMEOUT
- * (outputs: count 0, ids -1).  elis_peer_attach_local wires predictors that live in ONE process
+ * (outputs: count 0, ids -1).  The call counter lives in device memory (bumped by the kernel), so
+ * a sequence of calls may be captured in a CUDA graph and replayed on every rank.
+ * elis_peer_attach_local wires predictors that live in ONE process
  * (peers[r] = rank r; devices may repeat -- tests -- or differ, with peer access enabled). */
 elis_status elis_peer_export(elis_predictor* p, int32_t rank, int32_t world, void* out_handle64);
 elis_status elis_peer_attach(elis_predictor* p, const void* handles);

@@ -192,7 +192,7 @@ struct elis_predictor {
   uint8_t* peer_map[kMaxPeers] = {};
   bool peer_ipc[kMaxPeers] = {};   // mapped with cudaIpcOpenMemHandle (closed on destroy)
   bool use_peer = false;
-  uint32_t peer_epoch = 0;
+  uint32_t* peer_epoch = nullptr;  // device call counter of the peer select (see PeerArgs)
 
   // host-buffer iteration staging
   int32_t *d_tokens = nullptr, *d_lengths = nullptr, *d_generated = nullptr, *d_ids = nullptr, *d_count = nullptr;
@@ -742,7 +742,8 @@ static elis_status peer_check(elis_predictor* p, int32_t rank, int32_t world) {
 static elis_status peer_alloc_buffers(elis_predictor* p, int32_t rank, int32_t world) {
   CUDA_TRY(cudaSetDevice(p->device));
   if (!p->peer_own) {
-    if (p->alloc(&p->peer_own, peer_region_bytes()) != cudaSuccess) return fail(ELIS_ERR_OOM, "peer region");
+    if (p->alloc(&p->peer_own, peer_region_bytes()) != cudaSuccess || p->alloc(&p->peer_epoch, 1) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "peer region");
     CUDA_TRY(cudaDeviceSynchronize());  // the zeroed flags are in place before any peer maps it
   }
   if (!p->mkeys || p->world < world) {
@@ -761,6 +762,12 @@ elis_status elis_peer_export(elis_predictor* p, int32_t rank, int32_t world, voi
   if (!out_handle64) return fail(ELIS_ERR_INVALID_ARG, "NULL handle");
   s = peer_alloc_buffers(p, rank, world);
   if (s != ELIS_OK) return s;
+  // a fresh protocol: own flags and call counter at 0.  Done here, before the caller's handle
+  // all-gather (which no rank leaves before every rank has exported), never in attach: a faster
+  // rank may already be storing its first candidates into this region once it has attached.
+  CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes()));
+  CUDA_TRY(cudaMemset(p->peer_epoch, 0, sizeof(uint32_t)));
+  CUDA_TRY(cudaDeviceSynchronize());
   cudaIpcMemHandle_t h;
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
   CUDA_TRY(cudaIpcGetMemHandle(&h, p->peer_own));
@@ -792,7 +799,6 @@ elis_status elis_peer_attach(elis_predictor* p, const void* handles) {
     p->peer_ipc[r] = true;
   }
   p->use_peer = true;
-  p->peer_epoch = 0;
   return ELIS_OK;
 }
 
@@ -816,8 +822,10 @@ elis_status elis_peer_attach_local(elis_predictor* const* peers, int32_t world) 
       p->peer_ipc[q] = false;
       p->peer_map[q] = peers[q]->peer_own;
     }
+    CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes()));
+    CUDA_TRY(cudaMemset(p->peer_epoch, 0, sizeof(uint32_t)));
+    CUDA_TRY(cudaDeviceSynchronize());
     p->use_peer = true;
-    p->peer_epoch = 0;
   }
   return ELIS_OK;
 }
@@ -846,8 +854,7 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
     for (int r = 0; r < kMaxPeers; ++r) pa.region[r] = p->peer_map[r];
     pa.rank = p->rank;
     pa.world = p->world;
-    pa.epoch = ++p->peer_epoch;
-    if (pa.epoch == 0) pa.epoch = ++p->peer_epoch;  // never 0 (the regions' initial flag value)
+    pa.epoch = p->peer_epoch;
     LAUNCH(p, PC_ALLGATHER, st,
            launch_select_dist_peer(p->sc.keys, p->sc.info, n_local, batch_cap, global_offset, pa, running, p->mkeys,
                                    p->mids, out_ids, pre ? pre->out_count : nullptr,

@@ -182,7 +182,8 @@ constexpr int kMaxPeers = 8;
 struct PeerArgs {
   uint8_t* region[kMaxPeers];
   int rank, world;
-  uint32_t epoch;  // > 0, identical on every rank for the same call
+  uint32_t* epoch;  // this rank's call counter in device memory (the kernel bumps it): identical on
+                    // every rank for the same call, and no host state -- the call can be graph-captured
 };
 size_t peer_region_bytes();
 // local top-cap -> stores into every rank's region + release flags -> acquire every rank's

@@ -411,7 +411,9 @@ __global__ void __launch_bounds__(kSelThreads)
   int32_t* ci = reinterpret_cast<int32_t*>(ck + sort_len);                  // [sort_len]
   __shared__ int s_timeout;
   const int tid = threadIdx.x;
-  const int par = static_cast<int>(pa.epoch & 1u);
+  uint32_t epoch = *pa.epoch + 1u;
+  if (epoch == 0u) epoch = 1u;     // never 0: the regions' initial flag value
+  const int par = static_cast<int>(epoch & 1u);
   if (tid == 0) s_timeout = 0;
   // 1. this rank's top-cap (ids = local slot index)
   int elig = 0;
@@ -429,13 +431,13 @@ __global__ void __launch_bounds__(kSelThreads)
   __syncthreads();  // every thread's peer stores precede the fence + flag store below
   if (tid < pa.world) {
     __threadfence_system();
-    st_release_sys_u32(peer_flags(pa.region[tid], par) + pa.rank, pa.epoch);
+    st_release_sys_u32(peer_flags(pa.region[tid], par) + pa.rank, epoch);
   }
   // 3. acquire every rank's flag of this epoch (bounded: a missing rank sets ERR_PEER_TIMEOUT)
   if (tid < pa.world) {
     const uint32_t* f = peer_flags(pa.region[pa.rank], par) + tid;
     const unsigned long long t0 = peer_globaltimer();
-    while (static_cast<int32_t>(ld_acquire_sys_u32(f) - pa.epoch) < 0) {
+    while (static_cast<int32_t>(ld_acquire_sys_u32(f) - epoch) < 0) {
       __nanosleep(32);
       if (peer_globaltimer() - t0 > kPeerTimeoutNs) {
         atomicOr(err, ERR_PEER_TIMEOUT);
@@ -464,6 +466,7 @@ __global__ void __launch_bounds__(kSelThreads)
   for (int j = tid; j < cap; j += kSelThreads) out_ids[j] = j < got ? ci[j] : -1;
   const unsigned long long thr = got > 0 ? ck[got - 1] : 0ull;
   if (tid == 0) {
+    *pa.epoch = epoch;  // read by the next call's kernel (stream order)
     if (out_count) *out_count = got;
     if (out_nan) *out_nan = static_cast<int32_t>(local_info[6]);
     info[0] = static_cast<uint32_t>(thr);
