@@ -674,8 +674,10 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
     if (f16 && ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
     auto kern = f16 ? k_attention_tc<false, true> : ctx_f8_scale > 0.f ? k_attention_tc<true, false>
                                                                        : k_attention_tc<false, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
-    if (e != cudaSuccess) return e;
+    if (!attr_once(reinterpret_cast<const void*>(kern))) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
+      if (e != cudaSuccess) return e;
+    }
     kern<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
                                          static_cast<int>(plane_rows), ctx_f8_scale);
   } else if (d == 32) {

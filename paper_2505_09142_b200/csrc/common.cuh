@@ -9,6 +9,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #define ELIS_DEV __device__ __forceinline__
 
 namespace elis {
@@ -364,6 +368,18 @@ ELIS_DEV uint32_t pack_e4m3x4(float x0, float x1, float x2, float x3) {
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(x1), "f"(x0));  // a -> upper byte
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(x3), "f"(x2));
   return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+
+
+// Host: true if `fn`'s launch attributes were already set on the current device (then skip the
+// cudaFuncSetAttribute calls); records it otherwise.  Attributes are per device context.
+inline bool attr_once(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  return !done.insert({fn, dev}).second;
 }
 
 }  // namespace elis

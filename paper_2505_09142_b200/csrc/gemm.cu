@@ -595,8 +595,13 @@ template <int BN, int EPI, bool DEEP, int PREC = 0>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   using SP = SmemPlan<BN, EPI, DEEP, PREC>;
   auto kern = k_gemm_tc<BN, EPI, DEEP, PREC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  // launch attributes: set once per device (each cudaFuncSetAttribute costs ~1 us of host time)
+  const bool first = !attr_once(reinterpret_cast<const void*>(kern));
+  if (first) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SP::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+  }
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
   const int num_n = g.args.N / BN;
   const bool ln = EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID16_LN;
@@ -614,7 +619,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (csize > 8) {
+  if (first && csize > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }

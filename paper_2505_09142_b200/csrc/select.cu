@@ -516,12 +516,10 @@ cudaError_t launch_select_topk_nodes(const unsigned long long* keys, const int32
   if (num_nodes < 1 || num_nodes > kMaxNodes) return cudaErrorInvalidValue;
   const int sort_len = next_pow2(cap < 2 ? 2 : cap);
   const size_t smem = static_cast<size_t>(sort_len) * (sizeof(unsigned long long) + sizeof(int32_t));
-  static bool attr = false;
-  if (!attr) {
+  if (!attr_once(reinterpret_cast<const void*>(k_select_topk))) {  // per device
     cudaError_t e = cudaFuncSetAttribute(k_select_topk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kMaxBatchCap * 12 + 1024));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   k_select_topk<<<num_nodes, kSelThreads, smem, st>>>(keys, ids, node, node_ready, n, cap, out_ids, out_count,
                                                       out_nan, sc.info, node ? nullptr : sc.sel_keys,
@@ -574,12 +572,10 @@ cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32
     return cudaErrorInvalidValue;
   const int sort_len = next_pow2(cap < 2 ? 2 : cap);
   const size_t smem = static_cast<size_t>(sort_len) * (sizeof(unsigned long long) + sizeof(int32_t));
-  static bool attr = false;
-  if (!attr) {
+  if (!attr_once(reinterpret_cast<const void*>(k_select_dist_peer))) {  // per device
     cudaError_t e = cudaFuncSetAttribute(k_select_dist_peer, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kMaxBatchCap * 12 + 1024));
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   k_select_dist_peer<<<1, kSelThreads, smem, st>>>(keys, local_info, n_local, cap, global_offset, pa, running, mkeys,
                                                    mids, out_ids, out_count, out_nan, out_preempted, info, err,
