@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["elis", "reference"], default="elis")
     ap.add_argument("--config", choices=["tiny", "base", "large"], default="base")
-    ap.add_argument("--n", type=int, default=256, help="requests re-predicted per GPU per step")
+    ap.add_argument("--n", "--requests", dest="n", type=int, default=256,
+                    help="requests re-predicted per GPU per step (--requests: the same, for torchrun command lines, "
+                         "whose parser takes a bare --n for its own --nnodes / --nproc-per-node)")
     ap.add_argument("--lengths", default="trace", help="trace | uniform | fixed:L")
     ap.add_argument("--cap", type=int, default=4, help="batch_cap")
     ap.add_argument("--seed", type=int, default=0)
@@ -320,7 +322,21 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share_gpu():
+        local = 0
     return world, rank, local
+
+
+def share_gpu() -> bool:
+    """ELIS_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 with a gloo control plane, so the
+    N > 1 code path (peer-memory transport over CUDA IPC, barriers, max over ranks, the JSON line)
+    can be exercised on a one-GPU box.  Its timings are meaningless (the ranks share one GPU)."""
+    return os.environ.get("ELIS_BENCH_SHARE_GPU") == "1"
+
+
+def _ctl(t):
+    """Tensor for a control-plane collective: CUDA under NCCL, host memory under gloo."""
+    return t.cpu() if share_gpu() else t
 
 
 def run_reference(args):
@@ -367,7 +383,10 @@ def run_elis(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = encoder_cfg(args)
     W = inputs.make_weights(cfg, seed=0)
     st = torch.cuda.current_stream()
@@ -445,7 +464,7 @@ def run_elis(args):
                 ok = 1
             except binding.ElisError as e:
                 print(f"[rank {rank}] peer transport unavailable: {e}", file=sys.stderr)
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        flag = _ctl(torch.tensor([ok], dtype=torch.int32, device="cuda"))
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 1:
             args.transport_used = "peer (NVLink stores + epoch flags, fused select kernel)"
@@ -545,7 +564,7 @@ def run_elis(args):
     ms_step_profiled = evp[0].elapsed_time(evp[1]) / args.steps
     per_step = [ev[k].elapsed_time(ev_end[k]) for k in range(args.steps)]
     total_ms = sum(per_step) if flush else ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    t = _ctl(torch.tensor([total_ms], dtype=torch.float64, device="cuda"))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -586,7 +605,7 @@ def run_elis(args):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         e2e_step()
-    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    e2e_s = _ctl(torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda"))
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = world * n * args.steps / float(e2e_s.item())
