@@ -91,3 +91,21 @@ def test_residual16_config_rules(cuda_lib):
     flat = inputs.flatten_weights(cfg, inputs.make_weights(cfg, seed=0))
     with pytest.raises(binding.ElisError):
         binding.Predictor(cfg, flat, 1024, 8, precision="bf16", residual16=True)
+
+
+def test_residual16_cls_pooling_parity(cuda_lib):
+    """CLS pooling (P:138 reading) over the fp16 stream: the pooled row is read from the fp16
+    buffer (k_pool<__half>); fp16 operands hold CLS to the 1e-2 bar (DESIGN.md Tolerances)."""
+    from oracle import head as ohead
+    cfg = inputs.EncoderConfig(**{**inputs.CONFIGS["base"].to_dict(), "pooling": inputs.POOL_CLS})
+    W = inputs.make_weights(cfg, seed=0)
+    flat = inputs.flatten_weights(cfg, W)
+    L, _, _ = inputs.trace_lengths(16, seed=9)
+    L = L.astype(np.int32)
+    tokens = inputs.make_tokens(L, seed=9)
+    ref, hs = ohead.predict_with_hidden(tokens, L, W, cfg)
+    p, h = _run(cfg, flat, L, tokens, True)
+    rel = np.abs(p - ref) / np.maximum(np.abs(ref), 1.0)
+    print(f"CLS residual16: pred rel max {rel.max():.4g}; hidden max abs {np.abs(h - np.concatenate(hs)).max():.4g}")
+    assert rel.max() <= PRED_RTOL, rel.max()
+    assert np.abs(h - np.concatenate(hs)).max() <= HIDDEN_ATOL
