@@ -293,6 +293,14 @@ ELIS_DEV uint32_t mapa_shared(uint32_t local_addr, uint32_t rank) {
 ELIS_DEV void st_cluster_f32x2(uint32_t addr, float a, float b) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }
+// Asynchronous remote store that completes `8` transaction bytes on the destination CTA's mbarrier
+// (DSMEM producer -> consumer without a release fence: the consumer's wait on that barrier sees the
+// data).  Both addresses are shared::cluster addresses (mapa).
+ELIS_DEV void st_async_f32x2(uint32_t remote_addr, float a, float b, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "f"(a), "f"(b), "r"(remote_bar)
+               : "memory");
+}
 ELIS_DEV void mbar_arrive_remote_release(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }

@@ -236,7 +236,11 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EW);  // one arrive per epilogue warp of both CTAs (leader's copy used)
+#ifdef ELIS_LN_RELEASE_ARRIVES
       mbar_init(&sfull[a], 4 * cpairs);      // one arrive per half-0 epilogue warp of every row peer
+#else
+      mbar_init(&sfull[a], 1);               // the local expect_tx; the peers' st.async complete the bytes
+#endif
     }
     for (int i = 0; i < 2 * EW; ++i) mbar_init(&rfull[i], 1);
     fence_mbar_init();
@@ -511,14 +515,29 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
           chan_merge(cn, cmean, cm2, st_n, o.x, o.y);
           const uint32_t lslot = smem_u32(&stats[(slot * kMaxCluster + pair_in_cluster) * 128 + row_in_tile]);
           const uint32_t lbar = smem_u32(&sfull[slot]);
+#ifdef ELIS_LN_RELEASE_ARRIVES
           for (int pp = 0; pp < cpairs; ++pp)
             st_cluster_f32x2(mapa_shared(lslot, static_cast<uint32_t>(2 * pp + hrow)), cmean, cm2);
           __syncwarp();
           if (lane == 0)  // release is cumulative over the warp's DSMEM stores ordered by __syncwarp
             for (int pp = 0; pp < cpairs; ++pp)
               mbar_arrive_remote_release(mapa_shared(lbar, static_cast<uint32_t>(2 * pp + hrow)));
+#else
+          // st.async: each row's (mean, M2) lands in every row peer and completes 8 bytes on its
+          // barrier -- no release fence on the epilogue's critical path
+          for (int pp = 0; pp < cpairs; ++pp) {
+            const uint32_t r = static_cast<uint32_t>(2 * pp + hrow);
+            st_async_f32x2(mapa_shared(lslot, r), cmean, cm2, mapa_shared(lbar, r));
+          }
+#endif
         }
+#ifdef ELIS_LN_RELEASE_ARRIVES
         if (lane == 0) mbar_wait_acquire_cluster(&sfull[slot], sph);
+#else
+        // this CTA expects 128 rows x 8 bytes from each of the cpairs row peers (itself included)
+        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&sfull[slot], static_cast<uint32_t>(cpairs) * 128u * 8u);
+        if (lane == 0) mbar_wait(&sfull[slot], sph);
+#endif
         __syncwarp();
         if (gt_me) { const long long g2 = GT_CLK(); GT_ADD(6, g2 - g1); g1 = g2; }
         // merge the cpairs partials in pair order (identical on every CTA) -> mean, rstd
