@@ -48,10 +48,12 @@ elis_status elis_op_gemm_f8(const uint8_t* A, const uint8_t* W, const float* col
 
 /* fp16 residual stream variant (elis_config.residual16, EPI_BIAS_RESID16_LN): fp16 operands A, W;
  * v = A W^T + bias + resid_inout (fp16 [M, N], read as fp32); resid_inout <- fp16(LN(v)) in place
- * (statistics and normalisation in fp32).  N a multiple of 256, at most 1024. */
+ * (statistics and normalisation in fp32).  N a multiple of 256, at most 1024.  global_stats = 1
+ * (K >= 2048): the row statistics go through global memory between CTA pairs that share no cluster
+ * (the predictor's FFN2); the result is bit-identical to the cluster exchange. */
 elis_status elis_op_gemm_ln16(const uint16_t* A, const uint16_t* W, const float* bias, uint16_t* resid_inout,
                               const float* gamma, const float* beta, float eps, int32_t M, int32_t N, int32_t K,
-                              void* stream);
+                              int32_t global_stats, void* stream);
 /* FP8 variant of elis_op_gemm_ln: v = (A W^T) colscale + bias + resid_inout; resid_inout <- LN(v)
  * (fp32, in place), outb E4M3 bytes [M, N] = E4M3(out_scale * LN(v)).  N in {256, 512, 768, 1024}. */
 elis_status elis_op_gemm_ln_f8(const uint8_t* A, const uint8_t* W, const float* colscale, const float* bias,

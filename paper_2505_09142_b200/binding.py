@@ -105,7 +105,7 @@ def lib():
         "elis_op_gemm_ln": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _i32, _i32, _i32, _vp]),
         "elis_op_quant_rows_e4m3": (_i32, [_vp, _i32, _i32, _vp, _vp, _f32, _vp]),
         "elis_op_gemm_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32, _vp]),
-        "elis_op_gemm_ln16": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _vp]),
+        "elis_op_gemm_ln16": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]),
         "elis_op_gemm_ln_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _f32, _i32, _i32, _i32, _vp]),
         "elis_op_attention": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
         "elis_op_layernorm": (_i32, [_vp, _vp, _vp, _f32, _i64, _i32, _vp, _vp, _vp]),
@@ -315,12 +315,12 @@ def op_gemm_f8(A, W, colscale, bias, out, epilogue: int, out_scale: float = 1.0,
                                 out_scale, _stream(stream)), "elis_op_gemm_f8")
 
 
-def op_gemm_ln16(A, W, bias, resid_inout, gamma, beta, eps: float, stream=None):
+def op_gemm_ln16(A, W, bias, resid_inout, gamma, beta, eps: float, global_stats: bool = False, stream=None):
     """fp16 A [M, K], W [N, K]; resid_inout fp16 [M, N] <- LN(A W^T + bias + resid_inout) in place."""
     M, K = A.shape
     N = W.shape[0]
     check(lib().elis_op_gemm_ln16(_ptr(A), _ptr(W), _ptr(bias), _ptr(resid_inout), _ptr(gamma), _ptr(beta), eps,
-                                  M, N, K, _stream(stream)), "elis_op_gemm_ln16")
+                                  M, N, K, int(global_stats), _stream(stream)), "elis_op_gemm_ln16")
 
 
 def op_gemm_ln_f8(A, W, colscale, bias, resid_inout, gamma, beta, eps: float, outb, out_scale: float, stream=None):

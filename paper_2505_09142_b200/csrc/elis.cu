@@ -159,6 +159,8 @@ struct elis_predictor {
 
   // workspaces
   float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
+  float2* gx_stats = nullptr;  // FFN2 LN statistics through global memory (GemmArgs::gstats / gflag)
+  uint32_t* gx_flag = nullptr;
   float* fc_part = nullptr;    // head split-K partials (kFcPartCap floats) + tickets
   uint32_t* fc_ctr = nullptr;
   // CLS-only last layer (cfg.cls_last_layer): compact per-request rows [max_requests, *]
@@ -474,6 +476,13 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled (qkv) failed");
 
   // ---- GEMM plans (TMA descriptors over the fixed workspaces; M set per call)
+  // ELIS_GEMM_GX=0 keeps FFN2's LN statistics on the cluster (A/B of the global-memory exchange)
+  const bool gx_on = !(getenv("ELIS_GEMM_GX") && getenv("ELIS_GEMM_GX")[0] == '0');
+  if (cfg->residual16 && gx_on) {
+    const size_t mt = (static_cast<size_t>(T) + 255) / 256;
+    ALLOC(p->gx_stats, mt * (cfg->hidden / 256) * 2 * 128);
+    ALLOC(p->gx_flag, mt * 2);
+  }
   for (int l = 0; l < cfg->num_layers; ++l) {
     Layer& L = p->layers[l];
     // out-proj and FFN2 carry the residual add + LayerNorm in their epilogue (in place on h32)
@@ -505,6 +514,10 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     if (H / cfg->num_heads == 64) ok = ok && gemm_plan_set_head_major(&L.p_qkv, p->qkv, T);
     ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
          gemm_plan_set_ln(&L.p_ffn2, p->hb, L.ln2g, L.ln2b, cfg->ln_eps, T);
+    if (cfg->residual16 && gx_on) {  // FFN2 (long K, mainloop-bound): every SM, stats via global memory
+      L.p_ffn2.args.gstats = p->gx_stats;
+      L.p_ffn2.args.gflag = p->gx_flag;
+    }
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
   if (cfg->cls_last_layer) {  // the last layer's out-proj / FFN over the compact CLS rows
@@ -1070,7 +1083,7 @@ elis_status elis_op_gemm_ln(const uint16_t* A, const uint16_t* W, const float* b
 
 elis_status elis_op_gemm_ln16(const uint16_t* A, const uint16_t* W, const float* bias, uint16_t* resid_inout,
                               const float* gamma, const float* beta, float eps, int32_t M, int32_t N, int32_t K,
-                              void* stream) {
+                              int32_t global_stats, void* stream) {
   if (!A || !W || !bias || !resid_inout || !gamma || !beta || M < 1 || N < 256 || N % 256 || K < 64 || K % 64 ||
       N / 256 > 4)
     return fail(ELIS_ERR_INVALID_ARG, "gemm_ln16 arguments");
@@ -1080,6 +1093,21 @@ elis_status elis_op_gemm_ln16(const uint16_t* A, const uint16_t* W, const float*
       !gemm_plan_set_ln(&g, resid_inout, gamma, beta, eps, static_cast<uint64_t>(M)))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
   g.f16 = 1;
+  static float2* gs = nullptr;   // test entry: one process-wide exchange buffer (calls serialised)
+  static uint32_t* gf = nullptr;
+  static size_t gcap = 0;
+  if (global_stats) {
+    if (K < 2048) return fail(ELIS_ERR_INVALID_ARG, "global_stats needs K >= 2048 (the long-K LN GEMM)");
+    const size_t mt = (static_cast<size_t>(M) + 255) / 256;
+    if (mt * (N / 256) * 2 * 128 > gcap) {
+      if (gs) { cudaFree(gs); cudaFree(gf); }
+      gcap = mt * (N / 256) * 2 * 128;
+      CUDA_TRY(cudaMalloc(&gs, gcap * sizeof(float2)));
+      CUDA_TRY(cudaMalloc(&gf, mt * 2 * sizeof(uint32_t)));
+    }
+    g.args.gstats = gs;
+    g.args.gflag = gf;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -137,6 +137,17 @@ ELIS_DEV float gelu_fast(float x) {
   return x * r;
 }
 
+ELIS_DEV unsigned long long gx_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+ELIS_DEV uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Chan et al. merge of (count, mean, M2) partial statistics.
 ELIS_DEV void chan_merge(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
   const float n = n_a + n_b;
@@ -167,7 +178,10 @@ ELIS_DEV void stage_e4m3_row(uint8_t* b, int lane, const float (&v)[32], float s
 }
 
 // PREC: 0 bf16 operands, 1 E4M3 operands (kind::f8f6f4), 2 fp16 operands (16-bit outputs in fp16)
-template <int BN, int EPI, bool DEEP, int PREC>
+// GX (LN epilogues): row statistics exchanged through global memory (args.gstats / gflag) by CTA
+// pairs that need not share a cluster -- the grid spans every SM instead of the 132 that clusters
+// of 6 fill; the pairs of a row group work on the same m tile at the same step of the schedule.
+template <int BN, int EPI, bool DEEP, int PREC, bool GX = false>
 __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
@@ -214,16 +228,17 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
   const int num_k = K / BKE;
   // Cluster = (LN ? num_n : 1) pairs.  CTA rank r: pair r >> 1, half (row half / B half) r & 1.
   const int crank = static_cast<int>(cluster_ctarank());
-  const int cpairs = LN ? num_n : 1;
+  constexpr bool LNC = LN && !GX;          // LN statistics over the cluster (DSMEM)
+  const int cpairs = LNC ? num_n : 1;
   const int pair_in_cluster = crank >> 1;
   const int hrow = crank & 1;              // which 128-row half of the pair tile
   const bool leader = hrow == 0;
   const int leader_rank = crank & ~1;
   const int cid = static_cast<int>(blockIdx.x) / (2 * cpairs);
   const int ncl = static_cast<int>(gridDim.x) / (2 * cpairs);
-  const int num_iter_tiles = LN ? num_m : num_m * num_n;
+  const int num_iter_tiles = LNC ? num_m : num_m * num_n;
   auto tile_mn = [&](int t, int& m, int& n) {
-    if (LN) { m = t; n = pair_in_cluster; } else { m = t / num_n; n = t % num_n; }
+    if (LNC) { m = t; n = pair_in_cluster; } else { m = t / num_n; n = t % num_n; }
   };
 
   if (warp == 0 && lane == 0) {
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
       }
       ++nstore;
     };
-    if constexpr (LN) {
+    if constexpr (LNC) {
       stage_vectors(pair_in_cluster);
       named_bar_sync(1, EW * 32);
     }
@@ -386,8 +401,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
         for (int c = 0; c < NRES && c < CH; ++c) load_res(row0, n * BN + cbase + c * 32, c);
       }
       res_prefetched = false;
-      if constexpr (!LN) {
-        named_bar_sync(1, EW * 32);  // previous tile's readers of sbias are done
+      if constexpr (!LNC) {
+        named_bar_sync(1, EW * 32);  // previous tile's readers of sbias (sgam, sbet) are done
         stage_vectors(n);
         named_bar_sync(1, EW * 32);
       }
@@ -508,6 +523,38 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
         const uint32_t sph = (it >> 1) & 1;
         part[half * 128 + row_in_tile] = make_float2(st_mean, st_m2);
         named_bar_sync(2, EW * 32);
+        float tn = 0.f, tmean = 0.f, tm2 = 0.f;
+        if constexpr (GX) {
+          // this CTA's statistics -> global memory; one release (fence + counter) per CTA; every
+          // CTA of the row group then reads the num_n partials in n order (= the cluster order)
+          float2* gs = args.gstats + (static_cast<size_t>(m) * num_n * 2 + hrow) * 128;
+          uint32_t* flag = args.gflag + m * 2 + hrow;
+          if (half == 0) {
+            float cn = st_n, cmean = st_mean, cm2 = st_m2;
+            const float2 o = part[128 + row_in_tile];
+            chan_merge(cn, cmean, cm2, st_n, o.x, o.y);
+            gs[n * 2 * 128 + row_in_tile] = make_float2(cmean, cm2);
+          }
+          named_bar_sync(3, EW * 32);  // all epilogue warps: the half-0 stores precede the release
+          if (ew == 0 && lane == 0) {
+            __threadfence();
+            atomicAdd(flag, 1u);
+          }
+          if (lane == 0) {
+            const unsigned long long t0 = gx_globaltimer();
+            while (ld_acquire_gpu_u32(flag) < static_cast<uint32_t>(num_n)) {
+              __nanosleep(64);
+              if (gx_globaltimer() - t0 > 2000000000ull) break;  // a missing peer: wrong rows, no hang
+            }
+          }
+          __syncwarp();
+          for (int p = 0; p < num_n; ++p) {
+            const float2 s2 = __ldcg(gs + p * 2 * 128 + row_in_tile);
+            if (p == 0) { tn = static_cast<float>(BN); tmean = s2.x; tm2 = s2.y; }
+            else chan_merge(tn, tmean, tm2, static_cast<float>(BN), s2.x, s2.y);
+          }
+          if (gt_me) { const long long g2 = GT_CLK(); GT_ADD(6, g2 - g1); g1 = g2; }
+        } else {
         if (half == 0) {
           // this CTA's statistics over its BN columns -> every CTA holding the same rows
           float cn = st_n, cmean = st_mean, cm2 = st_m2;
@@ -541,12 +588,12 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
         __syncwarp();
         if (gt_me) { const long long g2 = GT_CLK(); GT_ADD(6, g2 - g1); g1 = g2; }
         // merge the cpairs partials in pair order (identical on every CTA) -> mean, rstd
-        float tn = 0.f, tmean = 0.f, tm2 = 0.f;
         for (int p = 0; p < cpairs; ++p) {
           const float2 s2 = stats[(slot * kMaxCluster + p) * 128 + row_in_tile];
           if (p == 0) { tn = static_cast<float>(BN); tmean = s2.x; tm2 = s2.y; }
           else chan_merge(tn, tmean, tm2, static_cast<float>(BN), s2.x, s2.y);
         }
+        }  // cluster exchange
         const float rstd = 1.0f / sqrtf(tm2 / tn + args.eps);
         tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
@@ -610,10 +657,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
   }
 }
 
-template <int BN, int EPI, bool DEEP, int PREC = 0>
+template <int BN, int EPI, bool DEEP, int PREC = 0, bool GX = false>
 cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   using SP = SmemPlan<BN, EPI, DEEP, PREC>;
-  auto kern = k_gemm_tc<BN, EPI, DEEP, PREC>;
+  auto kern = k_gemm_tc<BN, EPI, DEEP, PREC, GX>;
   cudaError_t e = cudaSuccess;
   // launch attributes: set once per device (each cudaFuncSetAttribute costs ~1 us of host time)
   const bool first = !attr_once(reinterpret_cast<const void*>(kern));
@@ -623,7 +670,7 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   }
   const int num_m = (g.args.M + 2 * BM - 1) / (2 * BM);
   const int num_n = g.args.N / BN;
-  const bool ln = EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID16_LN;
+  const bool ln = (EPI == EPI_BIAS_RESID_LN || EPI == EPI_BIAS_RESID16_LN) && !GX;  // cluster LN
   const int cpairs = ln ? num_n : 1;
   const int csize = 2 * cpairs;
   if (cpairs > kMaxCluster) return cudaErrorInvalidValue;
@@ -652,7 +699,14 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
     max_clusters[csize] = mc;
   }
   const int work = ln ? num_m : num_m * num_n;
-  const int ncl = work < max_clusters[csize] ? work : max_clusters[csize];
+  int ncl = work < max_clusters[csize] ? work : max_clusters[csize];
+  if constexpr (GX) {
+    // the num_n pairs of a row group take consecutive tiles: a multiple of num_n pairs keeps each
+    // group inside one step of the static schedule; the arrival counters start at 0
+    if (ncl >= num_n) ncl -= ncl % num_n;
+    e = cudaMemsetAsync(g.args.gflag, 0, static_cast<size_t>(num_m) * 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+  }
   cfg.gridDim = dim3(csize * ncl);
   e = cudaLaunchKernelEx(&cfg, kern, g.tmA, g.tmB, g.tmR, g.tmO, g.tmOb, g.args);
   if (e != cudaSuccess) return e;
@@ -682,6 +736,7 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
     if (!b256) return cudaErrorInvalidValue;
     switch (g.epi) {
       case EPI_BIAS_RESID16_LN:
+        if (deep && g.args.gstats) return launch_bn<256, EPI_BIAS_RESID16_LN, true, 2, true>(g, num_sms, st);
         return deep ? launch_bn<256, EPI_BIAS_RESID16_LN, true, 2>(g, num_sms, st)
                     : launch_bn<256, EPI_BIAS_RESID16_LN, false, 2>(g, num_sms, st);
       case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, 2>(g, num_sms, st);

@@ -31,6 +31,12 @@ struct GemmArgs {
   // and the LN epilogue's normalised copy are written as E4M3(out_scale * value)
   const float* colscale;
   float out_scale;
+  // LN row statistics through global memory instead of a cluster (EPI_BIAS_RESID16_LN, long K):
+  // the CTA pairs of one row group need not share a cluster, so the grid spans every SM.
+  // gstats [ceil(M/256)][N/256][2][128] float2, gflag [ceil(M/256)][2] arrival counters (zeroed
+  // before each launch); nullptr: the cluster / DSMEM exchange
+  float2* gstats;
+  uint32_t* gflag;
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major

@@ -199,3 +199,25 @@ def test_gemm_fused_residual16_layernorm_parity(cuda_lib, M, N, K):
     got = h.float().cpu().numpy().astype(np.float64)
     # one fp16 rounding of |y| <= ~6 (2^-9 relative) plus the fp32 accumulation
     np.testing.assert_allclose(got, ref, rtol=1.5e-3, atol=2e-4)
+
+
+@pytest.mark.parametrize("M", [1000, 43296, 77])
+def test_gemm_ln16_global_stats_bitwise_equal_cluster(cuda_lib, M):
+    """FFN2's LayerNorm statistics through global memory (CTA pairs without a shared cluster, the
+    grid on every SM) give bit-identical rows to the cluster / DSMEM exchange: the partials are
+    merged in the same n order."""
+    from paper_2505_09142_b200 import binding
+    rng = np.random.default_rng(M)
+    K, N = 3072, 768
+    A = torch.from_numpy(rng.normal(0, 1, (M, K))).half().cuda()
+    W = torch.from_numpy(rng.normal(0, 0.02, (N, K))).half().cuda()
+    res = torch.from_numpy(rng.normal(0.2, 1.5, (M, N))).half().cuda()
+    b = torch.from_numpy(rng.normal(0, 0.1, N).astype(np.float32)).cuda()
+    g = torch.from_numpy((1 + rng.uniform(-0.1, 0.1, N)).astype(np.float32)).cuda()
+    be = torch.from_numpy(rng.normal(0, 0.02, N).astype(np.float32)).cuda()
+    h_cl, h_gx = res.clone(), res.clone()
+    binding.op_gemm_ln16(A, W, b, h_cl, g, be, 1e-12, global_stats=False)
+    binding.op_gemm_ln16(A, W, b, h_gx, g, be, 1e-12, global_stats=True)
+    torch.cuda.synchronize()
+    assert torch.equal(h_cl, h_gx)
+    assert torch.isfinite(h_gx.float()).all()
