@@ -476,8 +476,11 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled (qkv) failed");
 
   // ---- GEMM plans (TMA descriptors over the fixed workspaces; M set per call)
-  // ELIS_GEMM_GX=0 keeps FFN2's LN statistics on the cluster (A/B of the global-memory exchange)
-  const bool gx_on = !(getenv("ELIS_GEMM_GX") && getenv("ELIS_GEMM_GX")[0] == '0');
+  // ELIS_GEMM_GX=1: FFN2's LN statistics through global memory, its CTA pairs on 144 SMs without a
+  // cluster (bit-identical).  Off by default: measured 2% slower than the 132-SM cluster exchange
+  // (FFN2 2.13 vs 2.10 ms per cfg2 step, scripts/_ab_gx.sh) -- the long-K GEMM is bound by operand
+  // traffic, not by the SM count
+  const bool gx_on = getenv("ELIS_GEMM_GX") && getenv("ELIS_GEMM_GX")[0] == '1';
   if (cfg->residual16 && gx_on) {
     const size_t mt = (static_cast<size_t>(T) + 255) / 256;
     ALLOC(p->gx_stats, mt * (cfg->hidden / 256) * 2 * 128);

@@ -1,4 +1,4 @@
-# A/B: FFN2 LN statistics through global memory on every SM (default) vs the 6-CTA cluster exchange
+# A/B: FFN2 LN statistics through global memory on 144 SMs (ELIS_GEMM_GX=1) vs the 6-CTA cluster exchange (default)
 timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "global_stats or residual16" 2>&1 | tail -2
 timeout 600 python -m pytest tests/test_gpu_residual16.py tests/test_gpu_predict.py -q -x -k "residual16 or r16" 2>&1 | tail -2
 for i in 1 2; do
