@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--cap", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--workers", default="1")
+    ap.add_argument("--precision", default=None, choices=["bf16", "fp16", "fp8"],
+                    help="encoder operands (default: fp16 + fp16 residual stream for head dim 64, as bench.py)")
     ap.add_argument("--aging", default="", help="boost_after,boost_amount (e.g. 4,50)")
     ap.add_argument("--sources", default="fcfs,isrtf_gpu,isrtf_noisy,isrtf_oracle")
     args = ap.parse_args()
@@ -47,7 +49,9 @@ def main():
         starv = {"boost_after": int(b), "boost_amount": float(a)}
     import torch
     cfg = inputs.CONFIGS[args.config]
-    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg, seed=0)), 512 * 64, 64)
+    prec = args.precision or ("fp16" if cfg.head_dim == 64 else "bf16")
+    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, inputs.make_weights(cfg, seed=0)), 512 * 64, 64,
+                          precision=prec, residual16=(prec == "fp16"))
     prompts, totals = inputs.stream_requests(args.n, seed=args.seed)
     lat = inputs.MODEL_AVG_LATENCY_MS["lam13"]
     ttft = 0.05 * lat
@@ -66,7 +70,8 @@ def main():
             f = res["fcfs"]["mean_jct_ms"]
             out = {"config": f"cfg4 stream: {args.n} Poisson requests, {W} workers, rate {m}x per worker "
                              f"({rate:.4f} req/s total), lam13 profile, cap {args.cap}, K 50, predictor {args.config} "
-                             f"on GPU" + (f", aging {starv}" if starv else ""),
+                             f"on GPU ({prec} operands{', fp16 residual' if prec == 'fp16' else ''})"
+                             + (f", aging {starv}" if starv else ""),
                    "workers": W, "rate_multiple": m, "results": res,
                    **{f"{k}_vs_fcfs_pct": 100.0 * (v["mean_jct_ms"] - f) / f for k, v in res.items() if k != "fcfs"},
                    "paper_context": "up to -19.6% average JCT vs FCFS with the trained predictor on A100 (P:30); "
