@@ -261,8 +261,9 @@ const char* elis_status_string(elis_status s);
 const char* elis_last_error(void);                 /* thread-local detail of the last failure */
 
 /* ---- instrumentation (bench / tests) ------------------------------------------------------ */
-/* Copy the final-layer fp32 hidden states [total_tokens, H] of the last predict call
- * (DEVICE dst, `count` floats >= total_tokens * H) -- parity tests compare them with the oracle. */
+/* Copy the final-layer hidden states [total_tokens, H] of the last predict call as fp32 (DEVICE
+ * dst, `count` floats >= total_tokens * H): the fp32 residual stream, or the fp16 stream widened
+ * when residual16 is set -- parity tests compare them with the oracle. */
 elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* stream);
 /* Number of kernels this predictor has launched so far. */
 uint64_t elis_launch_count(elis_predictor* p);
