@@ -109,3 +109,43 @@ def test_cls_last_layer_validation():
     assert L.elis_weight_count(ctypes.byref(mean)) == 0
     tiny = inputs.EncoderConfig(**{**inputs.CONFIGS["tiny"].to_dict(), "pooling": inputs.POOL_CLS})
     assert L.elis_weight_count(ctypes.byref(binding.make_config(tiny, 1024, 16, cls_last_layer=True))) == 0
+
+
+def _declared_arity():
+    """name -> number of parameters, parsed from the headers' prototypes."""
+    out = {}
+    for h in ("elis.h", "elis_ops.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(elis_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", src, flags=re.S):
+            params = m.group(2).strip()
+            out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_binding_signatures_match_the_headers():
+    """Every function the binding declares takes as many arguments as its C prototype (catches a
+    changed prototype the ctypes table did not follow)."""
+    L = binding.lib()
+    arity = _declared_arity()
+    checked = 0
+    for name, n in arity.items():
+        fn = getattr(L, name, None)
+        if fn is None or fn.argtypes is None:
+            continue
+        assert len(fn.argtypes) == n, (name, len(fn.argtypes), n)
+        checked += 1
+    assert checked >= 25
+
+
+def test_residual16_validation():
+    """residual16 (ABI v4) needs fp16 operands and no CLS-only last layer."""
+    L = binding.lib()
+    base = inputs.CONFIGS["base"]
+    ok = binding.make_config(base, 1024, 16, precision="fp16", residual16=True)
+    assert L.elis_weight_count(ctypes.byref(ok)) == inputs.weight_count(base)
+    bad = binding.make_config(base, 1024, 16, precision="bf16", residual16=True)
+    assert L.elis_weight_count(ctypes.byref(bad)) == 0
+    cls_cfg = inputs.EncoderConfig(**{**base.to_dict(), "pooling": inputs.POOL_CLS})
+    both = binding.make_config(cls_cfg, 1024, 16, precision="fp16", residual16=True, cls_last_layer=True)
+    assert L.elis_weight_count(ctypes.byref(both)) == 0
