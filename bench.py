@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--n", "--requests", dest="n", type=int, default=256,
                     help="requests re-predicted per GPU per step (--requests: the same, for torchrun command lines, "
                          "whose parser takes a bare --n for its own --nnodes / --nproc-per-node)")
+    ap.add_argument("--total-requests", type=int, default=0,
+                    help="strong scaling: this many requests re-predicted per step in total, split evenly over "
+                         "the GPUs (overrides --requests; the JSON line then says \"scaling\": \"strong\")")
     ap.add_argument("--lengths", default="trace", help="trace | uniform | fixed:L")
     ap.add_argument("--cap", type=int, default=4, help="batch_cap")
     ap.add_argument("--seed", type=int, default=0)
@@ -86,6 +89,13 @@ def encoder_cfg(args):
 
 
 def workload(args, rank: int):
+    if args.total_requests > 0:
+        # strong scaling: one request population for every N, rank r takes its contiguous slice
+        full = argparse.Namespace(**{**vars(args), "n": args.total_requests, "total_requests": 0})
+        L, gen, tokens = workload(full, 0)
+        offs = inputs.offsets(L)
+        a, b = rank * args.n, (rank + 1) * args.n
+        return L[a:b].copy(), gen[a:b].copy(), tokens[offs[a]:offs[b]].copy()
     n = args.n
     seed = args.seed * 1000 + rank
     if args.lengths == "trace":
@@ -381,6 +391,10 @@ def run_elis(args):
     world, rank, local = dist_env()
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.total_requests > 0:  # strong scaling: fixed total work split over the ranks
+        if args.total_requests % world:
+            raise SystemExit(f"--total-requests {args.total_requests} is not a multiple of {world} GPUs")
+        args.n = args.total_requests // world
     torch.cuda.set_device(local)
     if world > 1:
         if share_gpu():
@@ -619,7 +633,8 @@ def run_elis(args):
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "ms_per_step_p10_p50_p90": [round(float(np.percentile(per_step, q)), 4) for q in (10, 50, 90)],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.total_requests > 0 else "weak",
+            "vs_baseline": None,
             "dtype": {"bf16": "bf16", "fp16": "fp16",
                       "fp8": "fp8_e4m3 GEMMs (bf16 attention, fp32 residual/LN/head)"}[args.precision],
             "data": "synthetic (seeded trace-shaped lengths, uniform token ids, random-init BGE weights)",

@@ -49,3 +49,15 @@ def test_config_description_names_the_workload():
     a.transport_used = "peer (NVLink stores + epoch flags, fused select kernel)"
     d8 = bench.config_desc(a, 43296, 8)
     assert d8["transport"].startswith("peer") and "dp8" in d8["parallelism"]
+
+
+def test_strong_scaling_slices_one_population():
+    """--total-requests: every N sees the same request population; rank r's slice is contiguous."""
+    import numpy as np
+    a = _args("--total-requests", "64", "--config", "tiny")
+    a.n = 64
+    L, _, tok = bench.workload(a, 0)
+    a.n = 16
+    parts = [bench.workload(a, r) for r in range(4)]
+    np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), L)
+    np.testing.assert_array_equal(np.concatenate([p[2] for p in parts]), tok)

@@ -22,7 +22,8 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("extra", [[], ["--inflight", "4096", "--requests", "64"], ["--graph", "off"]])
+@pytest.mark.parametrize("extra", [[], ["--inflight", "4096", "--requests", "64"], ["--graph", "off"],
+                                   ["--total-requests", "32"]])
 def test_bench_two_ranks_peer_transport(cuda_lib, extra):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2", "--steps", "3",
@@ -35,5 +36,7 @@ def test_bench_two_ranks_peer_transport(cuda_lib, extra):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["config"]["transport"].startswith("peer"), d["config"]
+    if "--total-requests" in extra:
+        assert d["scaling"] == "strong" and d["config"]["requests_per_gpu"] == 16
     if "--graph" not in extra:
         assert d["config"]["cuda_graph"].startswith("on"), d["config"]
