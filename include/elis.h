@@ -228,7 +228,8 @@ elis_status elis_isrtf_select_dist(elis_predictor* p, const float* pred, const i
  *   2. the caller all-gathers the handles in rank order (e.g. torch.distributed);
  *   3. elis_peer_attach(p, handles): maps every other rank's region (HOST array world x 64 B).
  * From then on elis_isrtf_select_dist uses this transport.  Every rank must make the same
- * sequence of elis_isrtf_select_dist calls (like a collective); world <= 8.  A rank that never
+ * sequence of elis_isrtf_select_dist calls (like a collective) with the same batch_cap; n_local
+ * may differ per rank; world <= 8.  A rank that never
  * arrives makes the waiting ranks give up after 10 s with the sticky ELIS_ERR_PEER_TIMEOUT
  * (outputs: count 0, ids -1).  The call counter lives in device memory (bumped by the kernel), so
  * a sequence of calls may be captured in a CUDA graph and replayed on every rank.
