@@ -3,10 +3,13 @@
 // Owns the device weights (bf16 encoder matrices with Wq|Wk|Wv fused into one
 // [3H, H] operand, fp32 LN/bias/head), the workspace arena sized for
 // cfg.max_tokens / cfg.max_requests, the TMA descriptors of every encoder GEMM
-// (built once at create time: activation buffers never move), the NCCL
-// communicator and the instrumentation (launch counter, per-kernel CUDA-event
-// timing).  Every call enqueues on the caller's stream; nothing synchronises the
-// host except elis_sync_status / elis_iteration_host / elis_profile_read.
+// (built once at create time: activation buffers never move), the residual stream
+// (fp32 h32 + its 16-bit copy hb, or hb alone with cfg.residual16), the multi-GPU
+// exchange state (NCCL communicator, or the CUDA-IPC-mapped peer regions and the device
+// call counter of the peer-memory select) and the instrumentation (launch counter,
+// per-kernel CUDA-event timing).  Every call enqueues on the caller's stream; nothing
+// synchronises the host except elis_sync_status / elis_iteration_host /
+// elis_profile_read (and the one-time attach / export calls).
 #include <dlfcn.h>
 #include <nccl.h>
 
