@@ -484,6 +484,10 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   // (FFN2 2.13 vs 2.10 ms per cfg2 step, scripts/_ab_gx.sh) -- the long-K GEMM is bound by operand
   // traffic, not by the SM count
   const bool gx_on = getenv("ELIS_GEMM_GX") && getenv("ELIS_GEMM_GX")[0] == '1';
+  // M-tile order alternates along the layer chain (L2 reuse of the A rows the producer wrote last):
+  // QKV and FFN1 run descending.  Measured 8.12 -> 8.01 ms per cfg2 step (scripts/_ab_zigzag.sh);
+  // ELIS_GEMM_ZIGZAG=0 restores ascending order everywhere
+  const bool zigzag = !(getenv("ELIS_GEMM_ZIGZAG") && getenv("ELIS_GEMM_ZIGZAG")[0] == '0');
   if (cfg->residual16 && gx_on) {
     const size_t mt = (static_cast<size_t>(T) + 255) / 256;
     ALLOC(p->gx_stats, mt * (cfg->hidden / 256) * 2 * 128);
@@ -520,6 +524,10 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     if (H / cfg->num_heads == 64) ok = ok && gemm_plan_set_head_major(&L.p_qkv, p->qkv, T);
     ok = ok && gemm_plan_set_ln(&L.p_out, p->hb, L.ln1g, L.ln1b, cfg->ln_eps, T) &&
          gemm_plan_set_ln(&L.p_ffn2, p->hb, L.ln2g, L.ln2b, cfg->ln_eps, T);
+    if (zigzag) {  // QKV and FFN1 read their A operand in the reverse of the order it was written
+      L.p_qkv.args.m_reverse = 1;
+      L.p_ffn1.args.m_reverse = 1;
+    }
     if (cfg->residual16 && gx_on) {  // FFN2 (long K, mainloop-bound): every SM, stats via global memory
       L.p_ffn2.args.gstats = p->gx_stats;
       L.p_ffn2.args.gflag = p->gx_flag;

@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
   const int num_iter_tiles = LNC ? num_m : num_m * num_n;
   auto tile_mn = [&](int t, int& m, int& n) {
     if (LNC) { m = t; n = pair_in_cluster; } else { m = t / num_n; n = t % num_n; }
+    if (args.m_reverse) m = num_m - 1 - m;
   };
 
   if (warp == 0 && lane == 0) {

@@ -37,6 +37,9 @@ struct GemmArgs {
   // before each launch); nullptr: the cluster / DSMEM exchange
   float2* gstats;
   uint32_t* gflag;
+  // 1: M tiles in descending order, so a GEMM first reads the A rows its producer wrote last
+  // (still in L2) -- the producer / consumer chain alternates direction
+  int m_reverse;
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major
