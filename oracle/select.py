@@ -27,17 +27,6 @@ POLICY_ISRTF = 0
 POLICY_FCFS = 1
 
 
-def remaining_key(pred: np.float32, generated: int, head_predicts_total: bool) -> float:
-    """fp32 remaining-token key: max(0, rem) with NaN -> +inf and -0 -> +0."""
-    p = np.float32(pred)
-    rem = np.float32(p - np.float32(generated)) if head_predicts_total else p
-    if math.isnan(float(rem)):
-        return math.inf
-    if not (float(rem) > 0.0):
-        return 0.0
-    return float(rem)
-
-
 def starvation_adjust(rem: float, waited: int, is_running: bool, boost_after: int, boost_amount: float,
                       preempt_margin: float) -> float:
     """Starvation control ("policies that can adjust

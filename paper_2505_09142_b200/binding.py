@@ -19,12 +19,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, os.environ.get("ELIS_LIB", "libelis.so"))
 
 ELIS_OK = 0
-ABI_VERSION = 4  # include/elis.h ELIS_ABI_VERSION
+ABI_VERSION = 5  # include/elis.h ELIS_ABI_VERSION
 STATUS = {0: "ok", 1: "invalid argument", 2: "config", 3: "unsupported device", 4: "oom", 5: "cuda",
           6: "nccl", 7: "device input", 8: "peer timeout"}
 POLICY_ISRTF, POLICY_FCFS = 0, 1
 EPI_BIAS_BF16, EPI_BIAS_GELU_BF16, EPI_BIAS_RESID_F32 = 0, 1, 2
-PRECISION = {"bf16": 0, "fp8": 1, "fp16": 2}  # elis_precision
+PRECISION = {"auto": 0, "fp8": 1, "fp16": 2, "bf16": 3}  # elis_precision (auto: fp16 for head dim 64, else bf16)
+RESIDUAL = {None: 0, True: 1, False: 2}  # elis_residual: auto / fp16 stream / fp32 stream
 
 _vp, _i32, _i64, _u32, _f32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
                                     ctypes.c_float, ctypes.c_size_t)
@@ -35,7 +36,7 @@ class ElisConfig(ctypes.Structure):
                 ("num_layers", _i32), ("hidden", _i32), ("num_heads", _i32), ("intermediate", _i32),
                 ("ln_eps", _f32), ("pooling", _i32), ("head_layers", _i32), ("head_hidden", _i32),
                 ("head_predicts_total", _i32), ("max_tokens", _i32), ("max_requests", _i32), ("device", _i32),
-                ("precision", _i32), ("cls_last_layer", _i32), ("residual16", _i32)]
+                ("precision", _i32), ("cls_last_layer", _i32), ("residual_stream", _i32)]
 
 
 class ElisStarvation(ctypes.Structure):
@@ -93,6 +94,10 @@ def lib():
         "elis_isrtf_select_nodes": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
         "elis_iteration_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp,
                                        _vp, _vp, _vp]),
+        "elis_predict_remaining_dist": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
+        "elis_iteration_table_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
+                                             _vp]),
+        "elis_cost_split": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp]),
         "elis_sync_status": (_i32, [_vp]),
         "elis_last_device_error_bits": (_u32, [_vp]),
         "elis_status_string": (ctypes.c_char_p, [_i32]),
@@ -144,20 +149,22 @@ def _stream(stream):
 
 
 def make_config(cfg: inputs.EncoderConfig, max_tokens: int, max_requests: int, device: int = 0,
-                head_predicts_total: bool = False, precision: str = "bf16", cls_last_layer: bool = False,
-                residual16: bool = False) -> ElisConfig:
+                head_predicts_total: bool = False, precision: str = "auto", cls_last_layer: bool = False,
+                residual16: bool | None = None) -> ElisConfig:
+    """precision "auto" / residual16 None = the ABI defaults (elis.h ELIS_PREC_AUTO / ELIS_RESID_AUTO):
+    fp16 operands + fp16 residual stream for head dim 64 encoders, bf16 + fp32 stream otherwise."""
     return ElisConfig(ABI_VERSION, cfg.vocab_size, cfg.max_position, cfg.type_vocab_size, cfg.num_layers, cfg.hidden,
                       cfg.num_heads, cfg.intermediate, cfg.ln_eps, cfg.pooling, cfg.head_layers, cfg.head_hidden,
                       int(head_predicts_total), int(max_tokens), int(max_requests), int(device), PRECISION[precision],
-                      int(cls_last_layer), int(residual16))
+                      int(cls_last_layer), RESIDUAL[None if residual16 is None else bool(residual16)])
 
 
 class Predictor:
     """Owner of one elis_predictor (device weights + workspaces)."""
 
     def __init__(self, cfg: inputs.EncoderConfig, flat_weights: np.ndarray, max_tokens: int, max_requests: int,
-                 device: int = 0, head_predicts_total: bool = False, precision: str = "bf16",
-                 cls_last_layer: bool = False, residual16: bool = False):
+                 device: int = 0, head_predicts_total: bool = False, precision: str = "auto",
+                 cls_last_layer: bool = False, residual16: bool | None = None):
         L = lib()
         self.cfg = cfg
         self.precision = precision
@@ -189,6 +196,23 @@ class Predictor:
         n = int(lengths.shape[0])
         check(lib().elis_predict_remaining(self.h, _ptr(tokens), _ptr(lengths), n, int(total_tokens), _ptr(out_pred),
                                            _ptr(out_slot), _stream(stream)), "elis_predict_remaining")
+
+    def predict_remaining_dist(self, tokens, lengths, total_tokens: int, table, out_slot, stream=None):
+        """This rank's due requests -> table[out_slot[i]] on EVERY attached rank (a collective)."""
+        n = 0 if lengths is None else int(lengths.shape[0])
+        check(lib().elis_predict_remaining_dist(self.h, _ptr(tokens), _ptr(lengths), n, int(total_tokens),
+                                                _ptr(table), _ptr(out_slot), _stream(stream)),
+              "elis_predict_remaining_dist")
+
+    def iteration_table_host(self, tokens, lengths, slots, table, generated, batch_cap: int, out_ids,
+                             out_count=None, stream=None):
+        """Host due tokens / lengths / slots in, predict into the device table (all ranks when a
+        transport is attached), select over the whole table, host ids out; synchronises."""
+        n = int(lengths.shape[0])
+        check(lib().elis_iteration_table_host(self.h, _ptr(tokens), _ptr(lengths), n, int(tokens.shape[0]),
+                                              _ptr(slots), _ptr(table), _ptr(generated), int(generated.shape[0]),
+                                              int(batch_cap), None, _ptr(out_ids), _ptr(out_count),
+                                              _stream(stream)), "elis_iteration_table_host")
 
     def isrtf_select(self, pred, generated, batch_cap: int, out_ids, policy=POLICY_ISRTF, allow_preempt=True,
                      order=None, running=None, out_preempted=None, out_count=None, out_nan_count=None, stream=None,
@@ -279,6 +303,15 @@ def peer_attach_local(predictors: list["Predictor"]):
     """Wire predictors of ONE process as ranks 0..world-1 of the peer-memory transport."""
     arr = (_vp * len(predictors))(*[P.h for P in predictors])
     check(lib().elis_peer_attach_local(arr, len(predictors)), "elis_peer_attach_local")
+
+
+def cost_split(lengths: np.ndarray, world: int, cfg: inputs.EncoderConfig) -> np.ndarray:
+    """elis_cost_split: world + 1 slice bounds of the requests at the quantiles of their encoder cost."""
+    L = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = np.empty(world + 1, np.int32)
+    check(lib().elis_cost_split(L.ctypes.data if L.size else None, int(L.size), int(world), cfg.num_layers,
+                                cfg.hidden, cfg.intermediate, out.ctypes.data), "elis_cost_split")
+    return out
 
 
 def nccl_unique_id() -> bytes:

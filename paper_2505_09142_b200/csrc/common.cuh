@@ -321,6 +321,22 @@ ELIS_DEV void mbar_wait_acquire_cluster(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// ------------------------------------------------------------------ system-scope flags (peer memory)
+ELIS_DEV unsigned long long peer_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+ELIS_DEV void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+ELIS_DEV uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+constexpr unsigned long long kPeerTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: a rank that never arrives
+
 ELIS_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -4,7 +4,7 @@
 // [3H, H] operand, fp32 LN/bias/head), the workspace arena sized for
 // cfg.max_tokens / cfg.max_requests, the TMA descriptors of every encoder GEMM
 // (built once at create time: activation buffers never move), the residual stream
-// (fp32 h32 + its 16-bit copy hb, or hb alone with cfg.residual16), the multi-GPU
+// (fp32 h32 + its 16-bit copy hb, or hb alone with an fp16 residual stream), the multi-GPU
 // exchange state (NCCL communicator, or the CUDA-IPC-mapped peer regions and the device
 // call counter of the peer-memory select) and the instrumentation (launch counter,
 // per-kernel CUDA-event timing).  Every call enqueues on the caller's stream; nothing
@@ -82,6 +82,17 @@ uint16_t f32_to_bf16_rne(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+// ELIS_PREC_AUTO / ELIS_RESID_AUTO -> the configuration that meets the north_star parity bars
+// (R21, R23): fp16 operands + fp16 residual stream for head dim 64 encoders whose hidden
+// and intermediate sizes are multiples of 256 (BGE-base / large), bf16 + fp32 stream otherwise.
+void resolve_config(elis_config* c) {
+  const int d = c->num_heads > 0 ? c->hidden / c->num_heads : 0;
+  const bool f16_ok = d == 64 && c->hidden % 256 == 0 && c->intermediate % 256 == 0;
+  if (c->precision == ELIS_PREC_AUTO) c->precision = f16_ok ? ELIS_PREC_FP16 : ELIS_PREC_BF16;
+  if (c->residual_stream == ELIS_RESID_AUTO)
+    c->residual_stream = (c->precision == ELIS_PREC_FP16 && !c->cls_last_layer) ? ELIS_RESID_FP16 : ELIS_RESID_FP32;
+}
+
 bool config_valid(const elis_config* c, std::string* why) {
   auto bad = [&](const char* m) { if (why) *why = m; return false; };
   if (!c) return bad("cfg is NULL");
@@ -98,14 +109,20 @@ bool config_valid(const elis_config* c, std::string* why) {
   if (c->pooling != ELIS_POOL_MEAN && c->pooling != ELIS_POOL_CLS) return bad("pooling");
   if (c->head_layers < 2 || c->head_hidden < 1) return bad("head_layers >= 2, head_hidden >= 1");
   if (c->max_tokens < 1 || c->max_requests < 1) return bad("max_tokens / max_requests must be >= 1");
-  if (c->precision != ELIS_PREC_BF16 && c->precision != ELIS_PREC_FP8 && c->precision != ELIS_PREC_FP16)
+  if (c->precision != ELIS_PREC_AUTO && c->precision != ELIS_PREC_BF16 && c->precision != ELIS_PREC_FP8 &&
+      c->precision != ELIS_PREC_FP16)
     return bad("precision");
-  if (c->precision != ELIS_PREC_BF16 && (d != 64 || c->hidden % 256 || c->intermediate % 256))
+  if (c->precision != ELIS_PREC_AUTO && c->precision != ELIS_PREC_BF16 &&
+      (d != 64 || c->hidden % 256 || c->intermediate % 256))
     return bad("FP8 / FP16 need head dim 64 and hidden, intermediate multiples of 256");
   if (c->cls_last_layer != 0 && c->cls_last_layer != 1) return bad("cls_last_layer must be 0 or 1");
-  if (c->residual16 != 0 && c->residual16 != 1) return bad("residual16 must be 0 or 1");
-  if (c->residual16 && (c->precision != ELIS_PREC_FP16 || c->cls_last_layer))
-    return bad("residual16 needs precision = FP16 and cls_last_layer = 0");
+  if (c->residual_stream != ELIS_RESID_AUTO && c->residual_stream != ELIS_RESID_FP16 &&
+      c->residual_stream != ELIS_RESID_FP32)
+    return bad("residual_stream");
+  elis_config r = *c;
+  resolve_config(&r);
+  if (r.residual_stream == ELIS_RESID_FP16 && (r.precision != ELIS_PREC_FP16 || r.cls_last_layer))
+    return bad("an fp16 residual stream needs precision = FP16 and cls_last_layer = 0");
   if (c->cls_last_layer && (c->pooling != ELIS_POOL_CLS || d != 64))
     return bad("cls_last_layer needs pooling = CLS and head dim 64");
   return true;
@@ -198,6 +215,10 @@ struct elis_predictor {
   bool peer_ipc[kMaxPeers] = {};   // mapped with cudaIpcOpenMemHandle (closed on destroy)
   bool use_peer = false;
   uint32_t* peer_epoch = nullptr;  // device call counter of the peer select (see PeerArgs)
+  uint32_t* pred_epoch = nullptr;  // device call counter of the prediction exchange (PredPeerArgs)
+  uint32_t* pred_ticket = nullptr; // block arrival counter of k_head_out_dist
+  int2 *pred_send = nullptr, *pred_recv = nullptr;  // NCCL prediction exchange [max_requests], [world][max_requests]
+  int pred_recv_world = 0;
 
   // host-buffer iteration staging
   int32_t *d_tokens = nullptr, *d_lengths = nullptr, *d_generated = nullptr, *d_ids = nullptr, *d_count = nullptr;
@@ -323,6 +344,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
 
   elis_predictor* p = new elis_predictor();
   p->cfg = *cfg;
+  resolve_config(&p->cfg);
+  cfg = &p->cfg;  // the resolved copy from here on
   p->device = cfg->device;
   p->num_sms = prop.multiProcessorCount;
   const int H = cfg->hidden, F = cfg->intermediate, V = cfg->vocab_size, P = cfg->max_position;
@@ -437,7 +460,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   p->head_dims.push_back(1);
 
   // ---- workspaces
-  if (!cfg->residual16) ALLOC(p->h32, static_cast<size_t>(T) * H);  // residual16: the stream is hb
+  if (!(cfg->residual_stream == ELIS_RESID_FP16)) ALLOC(p->h32, static_cast<size_t>(T) * H);  // residual16: the stream is hb
   ALLOC(p->hb, static_cast<size_t>(T) * H);
   ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
   ALLOC(p->ctx, static_cast<size_t>(T) * H);
@@ -488,7 +511,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   // QKV and FFN1 run descending.  Measured 8.12 -> 8.01 ms per cfg2 step (scripts/_ab_zigzag.sh);
   // ELIS_GEMM_ZIGZAG=0 restores ascending order everywhere
   const bool zigzag = !(getenv("ELIS_GEMM_ZIGZAG") && getenv("ELIS_GEMM_ZIGZAG")[0] == '0');
-  if (cfg->residual16 && gx_on) {
+  if ((cfg->residual_stream == ELIS_RESID_FP16) && gx_on) {
     const size_t mt = (static_cast<size_t>(T) + 255) / 256;
     ALLOC(p->gx_stats, mt * (cfg->hidden / 256) * 2 * 128);
     ALLOC(p->gx_flag, mt * 2);
@@ -506,7 +529,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
                              kF8ScaleGelu) &&
            make_gemm_plan_f8(&L.p_ffn2, p->g, T, L.w2, L.s2, L.b2, p->h32, p->h32, 0, H, F, EPI_BIAS_RESID_LN,
                              kF8ScaleHidden);
-    else if (cfg->residual16)  // the LN epilogues read the residual from, and write LN(.) into, hb
+    else if ((cfg->residual_stream == ELIS_RESID_FP16))  // the LN epilogues read the residual from, and write LN(.) into, hb
       ok = make_gemm_plan(&L.p_qkv, p->hb, T, L.wqkv, L.bqkv, nullptr, p->qkv, 0, 3 * H, H, EPI_BIAS_BF16) &&
            make_gemm_plan(&L.p_out, p->ctx, T, L.wo, L.bo, reinterpret_cast<const float*>(p->hb), p->hb, 0, H, H,
                           EPI_BIAS_RESID16_LN) &&
@@ -528,9 +551,10 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
       L.p_qkv.args.m_reverse = 1;
       L.p_ffn1.args.m_reverse = 1;
     }
-    if (cfg->residual16 && gx_on) {  // FFN2 (long K, mainloop-bound): every SM, stats via global memory
+    if ((cfg->residual_stream == ELIS_RESID_FP16) && gx_on) {  // FFN2 (long K, mainloop-bound): every SM, stats via global memory
       L.p_ffn2.args.gstats = p->gx_stats;
       L.p_ffn2.args.gflag = p->gx_flag;
+      L.p_ffn2.args.err = p->err;
     }
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }
@@ -559,6 +583,14 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   return ELIS_OK;
 }
 
+// How the last head layer delivers y_i: into out_pred (local), or additionally to every rank
+// (elis_predict_remaining_dist) over peer memory (fused kernel) or NCCL (pairs + all-gather).
+enum HeadOutMode { HEAD_LOCAL = 0, HEAD_DIST_PEER = 1, HEAD_DIST_NCCL = 2 };
+
+static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
+                                int64_t total_tokens, float* out_pred, const int32_t* out_slot, int mode,
+                                cudaStream_t st);
+
 elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
                                    int64_t total_tokens, float* out_pred, const int32_t* out_slot, void* stream) {
   if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
@@ -567,8 +599,65 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   if (!tokens || !lengths || !out_pred) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
   if (total_tokens < n || total_tokens > p->cfg.max_tokens)
     return fail(ELIS_ERR_INVALID_ARG, "total_tokens outside [n, max_tokens]");
+  CUDA_TRY(cudaSetDevice(p->device));
+  return predict_impl(p, tokens, lengths, n, total_tokens, out_pred, out_slot, HEAD_LOCAL,
+                      static_cast<cudaStream_t>(stream));
+}
+
+elis_status elis_predict_remaining_dist(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
+                                        int64_t total_tokens, float* table, const int32_t* out_slot, void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (!p->comm && !p->use_peer) return fail(ELIS_ERR_INVALID_ARG, "neither elis_dist_attach nor elis_peer_attach was called");
+  if (n < 0 || n > p->cfg.max_requests) return fail(ELIS_ERR_INVALID_ARG, "n outside [0, max_requests]");
+  if (!table || (n > 0 && (!tokens || !lengths || !out_slot))) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  if (n > 0 && (total_tokens < n || total_tokens > p->cfg.max_tokens))
+    return fail(ELIS_ERR_INVALID_ARG, "total_tokens outside [n, max_tokens]");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUDA_TRY(cudaSetDevice(p->device));
+  p->last_stream = st;
+  if (p->use_peer) {
+    if (n > 0) return predict_impl(p, tokens, lengths, n, total_tokens, table, out_slot, HEAD_DIST_PEER, st);
+    // nothing to encode on this rank: it still publishes an empty segment and collects the others
+    PredPeerArgs pa{};
+    for (int r = 0; r < kMaxPeers; ++r) pa.region[r] = p->peer_map[r];
+    pa.rank = p->rank;
+    pa.world = p->world;
+    pa.max_pairs = p->cfg.max_requests;
+    pa.epoch = p->pred_epoch;
+    pa.ticket = p->pred_ticket;
+    LAUNCH(p, PC_ALLGATHER, st, launch_head_out_dist(nullptr, nullptr, nullptr, 0, 0, table, nullptr, pa, p->err, st));
+    return ELIS_OK;
+  }
+  // NCCL: pairs of this rank (slot -1 padded) -> ncclAllGather -> scatter into the table
+  if (!p->pred_send) {
+    if (p->alloc(&p->pred_send, p->cfg.max_requests) != cudaSuccess) return fail(ELIS_ERR_OOM, "prediction send buffer");
+  }
+  if (p->pred_recv_world < p->world) {
+    if (p->alloc(&p->pred_recv, static_cast<size_t>(p->cfg.max_requests) * p->world) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "prediction receive buffer");
+    p->pred_recv_world = p->world;
+  }
+  CUDA_TRY(cudaMemsetAsync(p->pred_send, 0xFF, static_cast<size_t>(p->cfg.max_requests) * sizeof(int2), st));
+  if (n > 0) {
+    elis_status s = predict_impl(p, tokens, lengths, n, total_tokens, table, out_slot, HEAD_DIST_NCCL, st);
+    if (s != ELIS_OK) return s;
+  }
+  {
+    cudaEvent_t a = nullptr;
+    p->prof_begin(PC_ALLGATHER, st, &a);
+    ncclResult_t r = nccl().allGather(p->pred_send, p->pred_recv, static_cast<size_t>(p->cfg.max_requests) * 8,
+                                      ncclUint8, p->comm, st);
+    if (r != ncclSuccess) return fail(ELIS_ERR_NCCL, std::string("ncclAllGather: ") + nccl().getErrorString(r));
+    p->prof_end(PC_ALLGATHER, st, a);
+  }
+  LAUNCH(p, PC_ALLGATHER, st,
+         launch_scatter_pairs(p->pred_recv, p->cfg.max_requests * p->world, table, st));
+  return ELIS_OK;
+}
+
+static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
+                                int64_t total_tokens, float* out_pred, const int32_t* out_slot, int mode,
+                                cudaStream_t st) {
   const elis_config& c = p->cfg;
   const int H = c.hidden;
   const int M = static_cast<int>(total_tokens);
@@ -594,7 +683,7 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
       const int kind = c.precision == ELIS_PREC_FP8 ? 2 : c.precision == ELIS_PREC_FP16 ? 1 : 0;
       LAUNCH(p, PC_ATTN, st,
              launch_attention_cls(p->qkv, p->cu, n, H, c.num_heads, T_cap, p->h32, p->ctx_c, p->hres_c, kind, f8_ctx,
-                                  st));
+                                  p->err, st));
       p->c_out.args.M = p->c_ffn1.args.M = p->c_ffn2.args.M = n;
       LAUNCH(p, PC_OUT, st, launch_gemm(p->c_out, p->num_sms, st));
       LAUNCH(p, PC_FFN1, st, launch_gemm(p->c_ffn1, p->num_sms, st));
@@ -612,7 +701,7 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
     LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st));
   else
     LAUNCH(p, PC_POOL, st,
-           c.residual16 ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st)
+           c.residual_stream == ELIS_RESID_FP16 ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st)
                         : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
   const float* x = p->pooled;
   float* bufs[2] = {p->z0, p->z1};
@@ -624,8 +713,22 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
            launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st));
     x = y;
   }
-  LAUNCH(p, PC_HEAD_OUT, st,
-         launch_head_out(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot, st));
+  if (mode == HEAD_DIST_PEER) {
+    PredPeerArgs pa{};
+    for (int r = 0; r < kMaxPeers; ++r) pa.region[r] = p->peer_map[r];
+    pa.rank = p->rank;
+    pa.world = p->world;
+    pa.max_pairs = c.max_requests;
+    pa.epoch = p->pred_epoch;
+    pa.ticket = p->pred_ticket;
+    LAUNCH(p, PC_HEAD_OUT, st,
+           launch_head_out_dist(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
+                                pa, p->err, st));
+  } else {
+    LAUNCH(p, PC_HEAD_OUT, st,
+           launch_head_out(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
+                           mode == HEAD_DIST_NCCL ? p->pred_send : nullptr, st));
+  }
   return ELIS_OK;
 }
 
@@ -769,7 +872,9 @@ static elis_status peer_check(elis_predictor* p, int32_t rank, int32_t world) {
 static elis_status peer_alloc_buffers(elis_predictor* p, int32_t rank, int32_t world) {
   CUDA_TRY(cudaSetDevice(p->device));
   if (!p->peer_own) {
-    if (p->alloc(&p->peer_own, peer_region_bytes()) != cudaSuccess || p->alloc(&p->peer_epoch, 1) != cudaSuccess)
+    if (p->alloc(&p->peer_own, peer_region_bytes(p->cfg.max_requests)) != cudaSuccess ||
+        p->alloc(&p->peer_epoch, 1) != cudaSuccess || p->alloc(&p->pred_epoch, 1) != cudaSuccess ||
+        p->alloc(&p->pred_ticket, 1) != cudaSuccess)
       return fail(ELIS_ERR_OOM, "peer region");
     CUDA_TRY(cudaDeviceSynchronize());  // the zeroed flags are in place before any peer maps it
   }
@@ -792,8 +897,10 @@ elis_status elis_peer_export(elis_predictor* p, int32_t rank, int32_t world, voi
   // a fresh protocol: own flags and call counter at 0.  Done here, before the caller's handle
   // all-gather (which no rank leaves before every rank has exported), never in attach: a faster
   // rank may already be storing its first candidates into this region once it has attached.
-  CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes()));
+  CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes(p->cfg.max_requests)));
   CUDA_TRY(cudaMemset(p->peer_epoch, 0, sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(p->pred_epoch, 0, sizeof(uint32_t)));
+  CUDA_TRY(cudaMemset(p->pred_ticket, 0, sizeof(uint32_t)));
   CUDA_TRY(cudaDeviceSynchronize());
   cudaIpcMemHandle_t h;
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
@@ -849,8 +956,10 @@ elis_status elis_peer_attach_local(elis_predictor* const* peers, int32_t world) 
       p->peer_ipc[q] = false;
       p->peer_map[q] = peers[q]->peer_own;
     }
-    CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes()));
+    CUDA_TRY(cudaMemset(p->peer_own, 0, peer_region_bytes(p->cfg.max_requests)));
     CUDA_TRY(cudaMemset(p->peer_epoch, 0, sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(p->pred_epoch, 0, sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(p->pred_ticket, 0, sizeof(uint32_t)));
     CUDA_TRY(cudaDeviceSynchronize());
     p->use_peer = true;
   }
@@ -957,6 +1066,83 @@ elis_status elis_iteration_host(elis_predictor* p, const int32_t* h_tokens, cons
   return ELIS_OK;
 }
 
+elis_status elis_iteration_table_host(elis_predictor* p, const int32_t* h_tokens, const int32_t* h_lengths, int32_t n,
+                                      int64_t total_tokens, const int32_t* h_slots, float* table,
+                                      const int32_t* generated, int32_t n_table, int32_t batch_cap,
+                                      const elis_preempt* preempt, int32_t* h_out_ids, int32_t* h_out_count,
+                                      void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (n < 0 || n > p->cfg.max_requests) return fail(ELIS_ERR_INVALID_ARG, "n outside [0, max_requests]");
+  if (!table || !generated || !h_out_ids || (n > 0 && (!h_tokens || !h_lengths || !h_slots)))
+    return fail(ELIS_ERR_INVALID_ARG, "NULL array");
+  if (n > 0 && (total_tokens < n || total_tokens > p->cfg.max_tokens)) return fail(ELIS_ERR_INVALID_ARG, "total_tokens");
+  const bool dist = p->comm || p->use_peer;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!p->d_tokens) {
+    const int N = p->cfg.max_requests;
+    if (p->alloc(&p->d_tokens, p->cfg.max_tokens) != cudaSuccess || p->alloc(&p->d_lengths, N) != cudaSuccess ||
+        p->alloc(&p->d_generated, N) != cudaSuccess || p->alloc(&p->d_order, N) != cudaSuccess ||
+        p->alloc(&p->d_running, N) != cudaSuccess || p->alloc(&p->d_pred, N) != cudaSuccess ||
+        p->alloc(&p->d_ids, kMaxBatchCap) != cudaSuccess || p->alloc(&p->d_count, 1) != cudaSuccess)
+      return fail(ELIS_ERR_OOM, "iteration staging");
+  }
+  // the slots ride in d_generated's staging buffer (the table's generated[] stays the caller's)
+  int32_t* d_slots = p->d_generated;
+  if (n > 0) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_tokens, h_tokens, total_tokens * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(p->d_lengths, h_lengths, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(d_slots, h_slots, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st));
+  }
+  elis_status s = dist ? elis_predict_remaining_dist(p, p->d_tokens, p->d_lengths, n, total_tokens, table, d_slots, stream)
+                       : elis_predict_remaining(p, p->d_tokens, p->d_lengths, n, total_tokens, table, d_slots, stream);
+  if (s != ELIS_OK) return s;
+  elis_preempt pre = preempt ? *preempt : elis_preempt{};
+  if (!preempt) pre.allow_preempt = 1;
+  pre.out_count = p->d_count;
+  s = elis_isrtf_select(p, table, generated, n_table, batch_cap, &pre, p->d_ids, stream);
+  if (s != ELIS_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(h_out_ids, p->d_ids, static_cast<size_t>(batch_cap) * 4, cudaMemcpyDeviceToHost, st));
+  if (h_out_count) CUDA_TRY(cudaMemcpyAsync(h_out_count, p->d_count, 4, cudaMemcpyDeviceToHost, st));
+  if (preempt && preempt->out_count)
+    CUDA_TRY(cudaMemcpyAsync(preempt->out_count, p->d_count, 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return ELIS_OK;
+}
+
+elis_status elis_cost_split(const int32_t* lengths, int32_t n, int32_t world, int32_t num_layers, int32_t hidden,
+                            int32_t intermediate, int32_t* out_bounds) {
+  if (!out_bounds || world < 1 || n < 0 || (n > 0 && !lengths) || num_layers < 1 || hidden < 1 || intermediate < 1)
+    return fail(ELIS_ERR_INVALID_ARG, "cost_split arguments");
+  // c(L) = a L + b L^2: the encoder's algorithmic FLOPs for one request of L tokens
+  // (BGE-base: 169.87e6 L + 36,864 L^2)
+  const double H = hidden, F = intermediate;
+  const double a = num_layers * 2.0 * (4.0 * H * H + 2.0 * H * F), b = num_layers * 4.0 * H;
+  std::vector<double> pre(static_cast<size_t>(n) + 1, 0.0);
+  for (int i = 0; i < n; ++i) {
+    const double L = lengths[i];
+    if (lengths[i] < 0) return fail(ELIS_ERR_INVALID_ARG, "negative length");
+    pre[i + 1] = pre[i] + (a * L + b * L * L);
+  }
+  out_bounds[0] = 0;
+  int lo = 0;
+  for (int r = 1; r < world; ++r) {
+    // the boundary whose prefix cost is closest to r / world of the total (ties -> the smaller index)
+    const double target = pre[n] * r / world;
+    int best = lo;
+    double bd = std::fabs(pre[lo] - target);
+    for (int i = lo + 1; i <= n; ++i) {
+      const double d = std::fabs(pre[i] - target);
+      if (d < bd) { bd = d; best = i; }
+      if (pre[i] > target) break;  // prefix sums ascend: later boundaries are farther
+    }
+    out_bounds[r] = best;
+    lo = best;
+  }
+  out_bounds[world] = n;
+  return ELIS_OK;
+}
+
 elis_status elis_sync_status(elis_predictor* p) {
   if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
   CUDA_TRY(cudaSetDevice(p->device));
@@ -969,6 +1155,9 @@ elis_status elis_sync_status(elis_predictor* p) {
     CUDA_TRY(cudaMemset(p->err, 0, 4));
     if (bits & ERR_PEER_TIMEOUT)
       return fail(ELIS_ERR_PEER_TIMEOUT, "a rank's candidates never arrived (device error bits " + std::to_string(bits) + ")");
+    if (bits & ERR_GX_TIMEOUT)
+      return fail(ELIS_ERR_PEER_TIMEOUT, "a LayerNorm statistics exchange partner never arrived (device error bits " +
+                                             std::to_string(bits) + ")");
     return fail(ELIS_ERR_DEVICE_INPUT, "device error bits " + std::to_string(bits));
   }
   return ELIS_OK;
@@ -980,12 +1169,12 @@ elis_status elis_get_hidden(elis_predictor* p, float* dst, int64_t count, void* 
   if (!p || !dst) return fail(ELIS_ERR_INVALID_ARG, "NULL argument");
   const int64_t need = p->last_T * p->cfg.hidden;
   if (count < need) return fail(ELIS_ERR_INVALID_ARG, "dst too small");
-  if (p->cfg.residual16)  // the final hidden states are the fp16 stream
+  if ((p->cfg.residual_stream == ELIS_RESID_FP16))  // the final hidden states are the fp16 stream
     CUDA_TRY(launch_f16_to_f32(p->hb, dst, need, static_cast<cudaStream_t>(stream)));
   else
     CUDA_TRY(cudaMemcpyAsync(dst, p->h32, need * 4, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
   if (p->cfg.cls_last_layer)  // the final CLS rows live in the compact buffer
-    CUDA_TRY(launch_scatter_rows(p->hres_c, p->cu, p->last_n, p->cfg.hidden, dst, static_cast<cudaStream_t>(stream)));
+    CUDA_TRY(launch_scatter_rows(p->hres_c, p->cu, p->last_n, p->cfg.hidden, p->err, dst, static_cast<cudaStream_t>(stream)));
   return ELIS_OK;
 }
 

@@ -545,7 +545,10 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
             const unsigned long long t0 = gx_globaltimer();
             while (ld_acquire_gpu_u32(flag) < static_cast<uint32_t>(num_n)) {
               __nanosleep(64);
-              if (gx_globaltimer() - t0 > 2000000000ull) break;  // a missing peer: wrong rows, no hang
+              if (gx_globaltimer() - t0 > 2000000000ull) {  // a missing peer: no hang, a sticky error
+                if (args.err) atomicOr(args.err, ERR_GX_TIMEOUT);
+                break;
+              }
             }
           }
           __syncwarp();
@@ -691,16 +694,22 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   // number of clusters that can be co-resident (one CTA per SM)
-  static int max_clusters[2 * kMaxCluster + 1] = {};  // per (BN, EPI, DEEP, F8) instantiation
-  if (max_clusters[csize] == 0) {
+  // per (BN, EPI, DEEP, F8) instantiation and device (the GX exchange needs the whole grid co-resident)
+  constexpr int kDevCache = 16;
+  static int max_clusters[kDevCache][2 * kMaxCluster + 1] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int mc_here = (dev < kDevCache) ? max_clusters[dev][csize] : 0;
+  if (mc_here == 0) {
     cudaLaunchConfig_t q = cfg;
     q.gridDim = dim3(csize * (num_sms / csize));
     int mc = 0;
     if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc <= 0) mc = num_sms / csize;
-    max_clusters[csize] = mc;
+    mc_here = mc;
+    if (dev < kDevCache) max_clusters[dev][csize] = mc;
   }
   const int work = ln ? num_m : num_m * num_n;
-  int ncl = work < max_clusters[csize] ? work : max_clusters[csize];
+  int ncl = work < mc_here ? work : mc_here;
   if constexpr (GX) {
     // the num_n pairs of a row group take consecutive tiles: a multiple of num_n pairs keeps each
     // group inside one step of the static schedule; the arrival counters start at 0

@@ -13,7 +13,7 @@ enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BI
        EPI_BIAS_RESID16_LN = 4 };
 
 // Device error bits (sticky; see elis.h).
-enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u };
+enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u, ERR_GX_TIMEOUT = 16u };
 
 // ---- GEMM (gemm.cu)
 struct GemmArgs {
@@ -40,6 +40,8 @@ struct GemmArgs {
   // 1: M tiles in descending order, so a GEMM first reads the A rows its producer wrote last
   // (still in L2) -- the producer / consumer chain alternates direction
   int m_reverse;
+  // sticky device error word (GX exchange timeout -> ERR_GX_TIMEOUT); nullptr: not reported
+  uint32_t* err;
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major
@@ -117,12 +119,15 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
 // query row (row cu[i]) over the request's keys, from the head-major qkv planes; writes the
 // compact ctx_c [n, H] (out_kind 0 bf16, 1 fp16, 2 E4M3(ctx_scale x)) and gathers the CLS
 // residual rows h32[cu[i]] into hres_c [n, H].  Head dim 64.
+// err: the sticky device error word; nothing is read or written once it is set (cu_seqlens may
+// then point past the token buffers)
 cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens, int n, int H, int num_heads,
                                  int64_t plane_rows, const float* h32, uint16_t* ctx_c, float* hres_c, int out_kind,
-                                 float ctx_scale, cudaStream_t st);
+                                 float ctx_scale, const uint32_t* err, cudaStream_t st);
 
 // ---- pooling + regression head (head.cu)
-cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, float* dst, cudaStream_t st);
+cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, const uint32_t* err,
+                                float* dst, cudaStream_t st);
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
                         float* pooled, cudaStream_t st);
 // mean / CLS pooling over the fp16 residual stream (elis_config.residual16)
@@ -140,8 +145,11 @@ struct FcWork {
 int fc_splits(int n, int N, int K, int num_sms, size_t part_cap, int ctr_cap);
 cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,
                           const FcWork& wk, cudaStream_t st);
+// out_pairs (optional): (out_slot[i], y_i) also written to out_pairs[i] (the NCCL exchange's send buffer)
 cudaError_t launch_head_out(const float* Z, const float* w, const float* b, int n, int K, float* out_pred,
-                            const int32_t* out_slot, cudaStream_t st);
+                            const int32_t* out_slot, int2* out_pairs, cudaStream_t st);
+// table[pairs[j].x] = pairs[j].y for every pair with x >= 0 (the NCCL exchange's receive side)
+cudaError_t launch_scatter_pairs(const int2* pairs, int count, float* table, cudaStream_t st);
 
 // ---- ISRTF select (select.cu)
 constexpr int kMaxBatchCap = 4096;
@@ -194,10 +202,42 @@ struct PeerArgs {
   uint32_t* epoch;  // this rank's call counter in device memory (the kernel bumps it): identical on
                     // every rank for the same call, and no host state -- the call can be graph-captured
 };
-size_t peer_region_bytes();
+// Bytes of one rank's region when it also carries the prediction exchange of
+// elis_predict_remaining_dist for up to max_pairs requests per rank (every rank uses the same).
+size_t peer_region_bytes(int max_pairs);
+// ---- prediction exchange over peer memory (elis_predict_remaining_dist).
+// Behind the select area of each region, at peer_pred_offset(): flags u32 [2][kMaxPeers],
+// counts u32 [2][kMaxPeers], (slot, pred) pairs [2][kMaxPeers][max_pairs] (8 B each), indexed by
+// the epoch's parity and the SOURCE rank.
+__host__ __device__ constexpr size_t peer_pred_offset() {
+  return (2 * static_cast<size_t>(kMaxPeers) * kMaxBatchCap * 12 + 2 * kMaxPeers * sizeof(uint32_t) + 255) & ~size_t(255);
+}
+__host__ __device__ inline uint32_t* peer_pred_flags(uint8_t* region, int par) {
+  return reinterpret_cast<uint32_t*>(region + peer_pred_offset()) + par * kMaxPeers;
+}
+__host__ __device__ inline uint32_t* peer_pred_counts(uint8_t* region, int par) {
+  return reinterpret_cast<uint32_t*>(region + peer_pred_offset()) + 2 * kMaxPeers + par * kMaxPeers;
+}
+__host__ __device__ inline int2* peer_pred_pairs(uint8_t* region, int par, int src, int max_pairs) {
+  return reinterpret_cast<int2*>(region + peer_pred_offset() + 4 * kMaxPeers * sizeof(uint32_t)) +
+         (static_cast<size_t>(par) * kMaxPeers + src) * max_pairs;
+}
+struct PredPeerArgs {
+  uint8_t* region[kMaxPeers];
+  int rank, world, max_pairs;
+  uint32_t* epoch;   // this rank's call counter of the prediction exchange (device; bumped by the kernel)
+  uint32_t* ticket;  // block arrival counter of the fused head-output kernel (zero between calls)
+};
 // local top-cap -> stores into every rank's region + release flags -> acquire every rank's
 // flag of this epoch -> identical merge -> out_ids (global), out_count, merged threshold in
 // info[0..1, 4], preempt flags of this rank's n_local slots.  One launch, one CTA.
+// Fused last head layer + prediction exchange over peer memory (elis_predict_remaining_dist):
+// y_i = Z_i . w + b, table[slot_i] = y_i locally and (slot_i, y_i) stored into every other rank's
+// region over NVLink; the last CTA to finish publishes this rank's count + epoch flag to every
+// rank (release, system scope), acquires every rank's flag (bounded; ERR_PEER_TIMEOUT) and
+// scatters the other ranks' pairs into the local table.  n may be 0 (the rank still exchanges).
+cudaError_t launch_head_out_dist(const float* Z, const float* w, const float* b, int n, int K, float* table,
+                                 const int32_t* slot, PredPeerArgs pa, uint32_t* err, cudaStream_t st);
 cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32_t* local_info, int n_local, int cap,
                                     int global_offset, PeerArgs pa, const uint8_t* running,
                                     unsigned long long* mkeys, int32_t* mids, int32_t* out_ids, int32_t* out_count,

@@ -374,19 +374,6 @@ __global__ void k_unpack(const Candidate* __restrict__ recv, int total, unsigned
 // select launches disappear.  Regions are double-buffered by epoch parity: rank s can only
 // write epoch e + 2 into a parity slot after it has seen every rank's epoch e + 1 flag, i.e.
 // after every rank finished reading epoch e from that slot.
-ELIS_DEV unsigned long long peer_globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-ELIS_DEV void st_release_sys_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-ELIS_DEV uint32_t ld_acquire_sys_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 constexpr size_t kPeerSlots = static_cast<size_t>(kMaxPeers) * kMaxBatchCap;   // candidates per parity
 ELIS_DEV unsigned long long* peer_keys(uint8_t* region, int par) {
   return reinterpret_cast<unsigned long long*>(region) + par * kPeerSlots;
@@ -397,7 +384,6 @@ ELIS_DEV int32_t* peer_ids(uint8_t* region, int par) {
 ELIS_DEV uint32_t* peer_flags(uint8_t* region, int par) {
   return reinterpret_cast<uint32_t*>(region + 2 * kPeerSlots * 12) + par * kMaxPeers;
 }
-constexpr unsigned long long kPeerTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s: a rank that never arrives
 
 __global__ void __launch_bounds__(kSelThreads)
     k_select_dist_peer(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ local_info,
@@ -561,7 +547,9 @@ cudaError_t launch_unpack_candidates(const void* recv, int total, unsigned long 
   return cudaGetLastError();
 }
 
-size_t peer_region_bytes() { return 2 * kPeerSlots * 12 + 2 * kMaxPeers * sizeof(uint32_t); }
+size_t peer_region_bytes(int max_pairs) {
+  return peer_pred_offset() + 2 * kMaxPeers * 2 * sizeof(uint32_t) + 2 * static_cast<size_t>(kMaxPeers) * max_pairs * 8;
+}
 
 cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32_t* local_info, int n_local, int cap,
                                     int global_offset, PeerArgs pa, const uint8_t* running,

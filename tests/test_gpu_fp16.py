@@ -14,12 +14,18 @@ torch = pytest.importorskip("torch")
 
 PRED_RTOL = 1e-2
 HIDDEN_ATOL = 2e-2
+# bf16 operands (elis.h ELIS_PREC_BF16, not the default): DESIGN.md R21 bounds their prediction
+# error by 8x the fp16 path's (bf16 keeps 8 significand bits, fp16 11: unit roundoff 2^-9 vs 2^-12)
+# -- 8 x 0.63% (the fp16 worst case) ~ 5%, measured 5.8%; the bar is 8% relative and 2 tokens
+# absolute.  The hidden-state bar is the north_star's 2e-2 (bf16 measured <= 0.019).
+BF16_PRED_RTOL = 8e-2
+BF16_PRED_ATOL_TOKENS = 2.0
 
 
 def _run(cfg, flat, L, tokens, precision):
     from paper_2505_09142_b200 import binding
     T = int(L.sum())
-    P = binding.Predictor(cfg, flat, T, len(L), precision=precision)
+    P = binding.Predictor(cfg, flat, T, len(L), precision=precision, residual16=False)
     out = torch.full((len(L),), float("nan"), device="cuda")
     P.predict_remaining(torch.from_numpy(tokens).cuda(), torch.from_numpy(L).cuda(), T, out)
     hid = torch.empty(T, cfg.hidden, device="cuda")
@@ -46,6 +52,12 @@ def test_predict_fp16_base_parity(cuda_lib, seed, n):
         rel = np.abs(p - ref) / np.maximum(np.abs(ref), 1.0)
         print(f"{prec}: pred rel max {rel.max():.4g} mean {rel.mean():.4g} abs max {np.abs(p - ref).max():.4g}; "
               f"hidden max abs {np.abs(h - ref_h).max():.4g}")
+    # bf16 is held to its own documented bound on the same (hardest measured) workload
+    pb, hb = res["bf16"]
+    rel_b = np.abs(pb - ref) / np.maximum(np.abs(ref), 1.0)
+    assert rel_b.max() <= BF16_PRED_RTOL, rel_b.max()
+    assert np.abs(pb - ref).max() <= BF16_PRED_ATOL_TOKENS, np.abs(pb - ref).max()
+    assert np.abs(hb - ref_h).max() <= HIDDEN_ATOL
     p16, h16 = res["fp16"]
     rel = np.abs(p16 - ref) / np.maximum(np.abs(ref), 1.0)
     assert rel.max() <= PRED_RTOL, rel.max()
@@ -65,7 +77,7 @@ def test_fp16_select_bit_exact(cuda_lib):
     L = L.astype(np.int32)
     tokens = inputs.make_tokens(L, seed=21)
     T = int(L.sum())
-    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, len(L), precision="fp16")
+    P = binding.Predictor(cfg, inputs.flatten_weights(cfg, W), T, len(L), precision="fp16", residual16=False)
     out = torch.empty(len(L), device="cuda")
     P.predict_remaining(torch.from_numpy(tokens).cuda(), torch.from_numpy(L).cuda(), T, out)
     ids = torch.empty(16, dtype=torch.int32, device="cuda")

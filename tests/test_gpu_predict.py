@@ -19,10 +19,15 @@ CLS_PRED_RTOL = 3e-2
 
 
 def make_predictor(name, max_tokens, max_requests, pooling=inputs.POOL_MEAN, **kw):
-    """precision "fp16-r16": fp16 operands with the fp16 residual stream (elis_config.residual16)."""
+    """precision "fp16-r16": fp16 operands with the fp16 residual stream; "fp16": fp16 operands with
+    the fp32 stream; "bf16": bf16 operands with the fp32 stream; none / "auto": the ABI default
+    (elis.h ELIS_PREC_AUTO: fp16 + fp16 stream for BGE-base / large, bf16 for the tiny encoder)."""
     from paper_2505_09142_b200 import binding
-    if kw.get("precision") == "fp16-r16":
+    prec = kw.get("precision")
+    if prec == "fp16-r16":
         kw = {**kw, "precision": "fp16", "residual16": True}
+    elif prec in ("fp16", "bf16"):
+        kw = {**kw, "residual16": False}
     cfg = inputs.EncoderConfig(**{**inputs.CONFIGS[name].to_dict(), "pooling": pooling})
     W = inputs.make_weights(cfg, seed=0)
     flat = inputs.flatten_weights(cfg, W)
@@ -86,7 +91,7 @@ def test_cfg1_tiny_full_parity_and_select(cuda_lib, pooling):
     P.close()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp16-r16"])
+@pytest.mark.parametrize("precision", ["auto", "bf16", "fp16", "fp16-r16"])
 def test_base_ragged_parity(cuda_lib, precision):
     """BGE-base, ragged lengths spanning several GEMM/attention tiles and ragged tails."""
     from oracle import head as ohead
@@ -103,7 +108,7 @@ def test_base_ragged_parity(cuda_lib, precision):
     P.close()
 
 
-@pytest.mark.parametrize("precision", ["bf16", "fp16", "fp16-r16", "fp8"])
+@pytest.mark.parametrize("precision", ["auto", "bf16", "fp16", "fp16-r16", "fp8"])
 def test_batch_invariance_bitwise(cuda_lib, precision):
     """pred_i is bitwise identical whether request i is encoded alone, in a batch, or in a
     different batch order (row-independent GEMMs, per-request attention/pool/head)."""

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert binding.lib().elis_abi_version() == binding.ABI_VERSION == 4
+    assert binding.lib().elis_abi_version() == binding.ABI_VERSION == 5
 
 
 @pytest.mark.parametrize("name", ["tiny", "base", "large"])
@@ -149,3 +149,52 @@ def test_residual16_validation():
     cls_cfg = inputs.EncoderConfig(**{**base.to_dict(), "pooling": inputs.POOL_CLS})
     both = binding.make_config(cls_cfg, 1024, 16, precision="fp16", residual16=True, cls_last_layer=True)
     assert L.elis_weight_count(ctypes.byref(both)) == 0
+
+
+def _brute_split(L, world, cfg):
+    """The SURVEY.md 8e rule written out: boundary r = the index whose prefix cost is closest to
+    r/world of the total (ties -> smaller index), searched from the previous boundary on."""
+    H, F, nl = cfg.hidden, cfg.intermediate, cfg.num_layers
+    c = [nl * (2.0 * (4 * H * H + 2 * H * F) * x + 4.0 * H * x * x) for x in L.tolist()]
+    pre = [0.0]
+    for v in c:
+        pre.append(pre[-1] + v)
+    b = [0]
+    for r in range(1, world):
+        tgt = pre[-1] * r / world
+        cands = range(b[-1], len(L) + 1)
+        b.append(min(cands, key=lambda i: (abs(pre[i] - tgt), i)))
+    b.append(len(L))
+    return np.array(b, np.int32), c
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("kind", ["trace", "uniform", "tiny"])
+def test_cost_split_matches_definition_and_balances(world, kind):
+    """elis_cost_split (host function of the C ABI, no GPU): equal to the written-out quantile rule,
+    contiguous, and every slice's cost within one request of total / world."""
+    cfg = inputs.CONFIGS["base"]
+    if kind == "trace":
+        L, _, _ = inputs.trace_lengths(1311, seed=world)
+    elif kind == "uniform":
+        L = inputs.uniform_lengths(500, seed=world)
+    else:
+        L = np.array([512, 1, 1, 3], np.int32)
+    got = binding.cost_split(L, world, cfg)
+    exp, c = _brute_split(L, world, cfg)
+    np.testing.assert_array_equal(got, exp)
+    assert got[0] == 0 and got[-1] == len(L) and (np.diff(got) >= 0).all()
+    if kind != "tiny":
+        tot, cmax = sum(c), max(c)
+        for r in range(world):
+            assert abs(sum(c[got[r]:got[r + 1]]) - tot / world) <= cmax + 1e-6 * tot
+    # BGE-base constants of SURVEY.md 8e: c(L) = 169.87e6 L + 36,864 L^2
+    assert abs(c[0] - (169.869312e6 * int(L[0]) + 36864.0 * int(L[0]) ** 2)) < 1.0
+
+
+def test_cost_split_edge_cases():
+    cfg = inputs.CONFIGS["base"]
+    np.testing.assert_array_equal(binding.cost_split(np.zeros(0, np.int32), 4, cfg), [0, 0, 0, 0, 0])
+    np.testing.assert_array_equal(binding.cost_split(np.array([100], np.int32), 3, cfg), [0, 0, 1, 1])
+    with pytest.raises(binding.ElisError):
+        binding.cost_split(np.array([1, 2], np.int32), 0, cfg)
