@@ -133,12 +133,19 @@ def test_predict_dist_base_default_precision_vs_oracle(cuda_lib):
     assert 0 < b[1] < len(L)
     streams = [torch.cuda.Stream() for _ in range(2)]
     tables = [torch.full((F,), SENTINEL, device="cuda") for _ in range(2)]
-    torch.cuda.synchronize()
+    # every rank's device inputs stay referenced until both ranks finished: a temporary freed after
+    # the call returns could be handed to the other rank's next allocation (another stream) while
+    # this rank's kernels still read it
+    args = []
     for r in range(2):
         a, e = b[r], b[r + 1]
         t = tok[offs[a]:offs[e]]
-        Ps[r].predict_remaining_dist(torch.from_numpy(t).cuda(), torch.from_numpy(L[a:e].copy()).cuda(), int(t.size),
-                                     tables[r], torch.from_numpy(slots[a:e].copy()).cuda(), stream=streams[r])
+        args.append((torch.from_numpy(t).cuda(), torch.from_numpy(L[a:e].copy()).cuda(), int(t.size),
+                     torch.from_numpy(slots[a:e].copy()).cuda()))
+    torch.cuda.synchronize()
+    for r in range(2):
+        t, l, T, s = args[r]
+        Ps[r].predict_remaining_dist(t, l, T, tables[r], s, stream=streams[r])
     torch.cuda.synchronize()
     for r in range(2):
         assert Ps[r].sync_status() == 0
