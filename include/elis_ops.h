@@ -68,6 +68,10 @@ elis_status elis_op_gemm_ln_f8(const uint8_t* A, const uint8_t* W, const float* 
  * softmax(Q_h K_h^T / sqrt(d)) V_h over the request's own L_i tokens.  d = H / num_heads in {32, 64}. */
 elis_status elis_op_attention(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T,
                               int32_t hidden, int32_t num_heads, uint16_t* ctx, void* stream);
+/* The same with fp16 planes and fp16 ctx (elis_config.precision = ELIS_PREC_FP16; P rounded to
+ * fp16).  d = 64 only. */
+elis_status elis_op_attention_f16(const uint16_t* qkv, const int32_t* lengths, int32_t n, int64_t T,
+                                  int32_t hidden, int32_t num_heads, uint16_t* ctx, void* stream);
 
 /* Row LayerNorm: y = (u - mean) / sqrt(var + eps) * gamma + beta (population variance).
  * u f32 [rows, H] -> out_f32 [rows, H] and (if non-NULL) out_bf16 [rows, H]; H in {128, 768, 1024}. */

@@ -113,6 +113,7 @@ def lib():
         "elis_op_gemm_ln16": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _vp]),
         "elis_op_gemm_ln_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _f32, _i32, _i32, _i32, _vp]),
         "elis_op_attention": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
+        "elis_op_attention_f16": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp, _vp]),
         "elis_op_layernorm": (_i32, [_vp, _vp, _vp, _f32, _i64, _i32, _vp, _vp, _vp]),
         "elis_op_fc_f32": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
     }
@@ -364,9 +365,10 @@ def op_gemm_ln_f8(A, W, colscale, bias, resid_inout, gamma, beta, eps: float, ou
           "elis_op_gemm_ln_f8")
 
 
-def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None):
-    check(lib().elis_op_attention(_ptr(qkv), _ptr(lengths), int(lengths.shape[0]), int(ctx.shape[0]), hidden,
-                                  num_heads, _ptr(ctx), _stream(stream)), "elis_op_attention")
+def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None, f16: bool = False):
+    fn = lib().elis_op_attention_f16 if f16 else lib().elis_op_attention
+    check(fn(_ptr(qkv), _ptr(lengths), int(lengths.shape[0]), int(ctx.shape[0]), hidden, num_heads, _ptr(ctx),
+             _stream(stream)), "elis_op_attention_f16" if f16 else "elis_op_attention")
 
 
 def op_layernorm(u, gamma, beta, eps: float, out32, outb=None, stream=None):

@@ -95,6 +95,80 @@ def test_attention_varlen_parity(cuda_lib, d, nh):
         assert err < 2e-2, (i, int(L), err)
 
 
+def fp16_tensor(x: np.ndarray):
+    """fp16-representable fp32 numpy -> (torch fp16 on cuda, exact fp64 numpy copy)."""
+    t = torch.from_numpy(np.asarray(x, np.float32)).to(torch.float16)
+    return t.cuda(), t.float().numpy().astype(np.float64)
+
+
+# lengths that exercise the packed short-request tiles (several requests of <= 128 tokens per
+# 128-row tile in 32-row segments, segment tails, a full pack of four 1..32-token requests) next to
+# long requests with a partial last q tile / key block
+PACK_LENGTHS = [1, 2, 31, 32, 33, 63, 64, 65, 96, 97, 127, 128, 129, 7, 512, 200, 33, 5, 9, 17, 30, 511, 256, 257,
+                100, 28, 3]
+
+
+@pytest.mark.parametrize("f16", [False, True])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_attention_packed_parity(cuda_lib, f16, seed):
+    """BGE-base attention (d = 64, 12 heads) on ragged lengths, bf16 and fp16 planes: every request
+    of every pack vs the fp64 oracle.  Tolerance: P and ctx rounded to 16 bits (2^-8 relative for
+    bf16, 2^-11 for fp16) on values of O(1)."""
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    H, nh = 768, 12
+    rng = np.random.default_rng(100 + seed)
+    lengths = np.array(PACK_LENGTHS, np.int32)
+    if seed:
+        rng.shuffle(lengths)
+    T = int(lengths.sum())
+    x = rng.normal(0, 1.0, (T, 3 * H))
+    qkv, qkv64 = fp16_tensor(x) if f16 else bf16_tensor(x)
+    ctx = torch.full((T, H), float("nan"), dtype=torch.float16 if f16 else torch.bfloat16, device="cuda")
+    binding.op_attention(attn_layout(qkv, H, nh), torch.from_numpy(lengths).cuda(), H, nh, ctx, f16=f16)
+    torch.cuda.synchronize()
+    got = to_np(ctx)
+    starts = inputs.offsets(lengths)
+    tol = 4e-3 if f16 else 2e-2
+    for i, L in enumerate(lengths):
+        sl = slice(starts[i], starts[i + 1])
+        ref = oenc.attention(qkv64[sl, :H], qkv64[sl, H:2 * H], qkv64[sl, 2 * H:], nh)
+        err = np.abs(got[sl] - ref).max()
+        assert err < tol, (i, int(L), err)
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_attention_batch_invariant_across_packs(cuda_lib, f16):
+    """A request's ctx is bitwise the same alone, at any 32-row segment of a pack and after a long
+    request (its keys are the same 32-key chunks in the same order wherever it lands)."""
+    from paper_2505_09142_b200 import binding
+    H, nh = 768, 12
+    rng = np.random.default_rng(7)
+    probe = np.array([20, 45, 90, 128], np.int32)   # 1, 2, 3 and 4 segments
+    x = rng.normal(0, 1.0, (int(probe.sum()), 3 * H))
+    mk = fp16_tensor if f16 else bf16_tensor
+    dt = torch.float16 if f16 else torch.bfloat16
+
+    def run(lengths, xx):
+        qkv, _ = mk(xx)
+        ctx = torch.zeros((int(lengths.sum()), H), dtype=dt, device="cuda")
+        binding.op_attention(attn_layout(qkv, H, nh), torch.from_numpy(lengths).cuda(), H, nh, ctx, f16=f16)
+        torch.cuda.synchronize()
+        return ctx.cpu()
+
+    po = inputs.offsets(probe)
+    alone = [run(probe[i:i + 1], x[po[i]:po[i + 1]]) for i in range(len(probe))]
+    fill = rng.normal(0, 1.0, (600, 3 * H))
+    for prefix in ([], [5], [33], [70], [31, 1], [300], [3, 3, 3]):
+        pre = np.array(prefix, np.int32)
+        for i in range(len(probe)):
+            L = np.concatenate([pre, probe[i:i + 1], np.array([9], np.int32)]).astype(np.int32)
+            npre = int(pre.sum())
+            xx = np.concatenate([fill[:npre], x[po[i]:po[i + 1]], fill[npre:npre + 9]])
+            got = run(L, xx)[npre:npre + int(probe[i])]
+            assert torch.equal(got.view(torch.int16), alone[i].view(torch.int16)), (prefix, int(probe[i]))
+
+
 def test_attention_single_token_is_v(cuda_lib):
     """L = 1 closed form on the GPU: ctx = v (up to bf16 of a bf16 value: exact)."""
     from paper_2505_09142_b200 import binding
