@@ -3,13 +3,13 @@
 // For every request i and head h (BERT self-attention,
 // P:42 "process tokens in parallel"):
 //     ctx_h = softmax(Q_h K_h^T / sqrt(d)) V_h   over the request's own L_i tokens,
-// no causal mask, no cross-request attention, no padding: the work list (k_meta) holds the
-// q tiles of the long requests and packs of short ones, so ragged lengths cost at most one
-// partial 32-row segment per request.
+// no causal mask, no cross-request attention, no padding: the work list holds one
+// 64-row query tile per (request, q0) so ragged lengths cost at most one partial tile.
 //
-// Head dim 64 (BGE-base / large): the persistent tcgen05 engine below.  Head dim 32 (the tiny
-// test encoder): flash-style online softmax on mma.sync m16n8k16 (fp32 statistics, exp2 with
-// the log2(e)/sqrt(d) scale folded in, P rounded to bf16 for the PV product), 64-row tiles.
+// v1 engine: flash-style online softmax (fp32 statistics, exp2 with the log2(e)/sqrt(d)
+// scale folded in), Q/K/V staged in shared memory with cp.async double buffering,
+// products on mma.sync m16n8k16 bf16 -> fp32 (P rounded to bf16 for the PV product).
+// The whole K/V of one (request, head) is <= 512 x 64 x 2 x 2 B = 128 KB.
 
 #include <algorithm>
 
@@ -19,36 +19,36 @@
 namespace elis {
 
 #ifdef ELIS_ATTN_TRACE
-// Diagnostic build only (python -m paper_2505_09142_b200.build --variant=atrace -DELIS_ATTN_TRACE):
-// %globaltimer stamps of the persistent engine's phases, per pipeline (CTA, pp): event code in the
-// low 8 bits (scripts/attn_trace.py decodes them).
-constexpr int kTrPipes = 512, kTrEvents = 2048;
-__device__ unsigned long long g_attn_trace[kTrPipes * kTrEvents];
-__device__ unsigned g_attn_trace_n[kTrPipes * 4];
-// the stamping thread keeps its event count in a register (a global counter's load would add an
-// L2 round trip to every stamp); the counts are stored once at the end
-ELIS_DEV void attn_tr(int pipe, int role, unsigned code, unsigned& k) {
+// Diagnostic build only (python -m paper_2505_09142_b200.build --variant=trace -DELIS_ATTN_TRACE):
+// thread 0 of every tcgen05 attention CTA stamps %globaltimer at its phase boundaries.
+constexpr size_t kTraceCap = 1 << 16;
+__device__ unsigned long long g_attn_trace[kTraceCap * 8];
+static void* g_attn_trace_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_attn_trace);
+  return p;
+}
+#define ATTN_TRACE(slot, val)                                                          \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      const size_t id_ = blockIdx.x;      \
+      if (id_ < kTraceCap) g_attn_trace[id_ * 8 + (slot)] = (val);                     \
+    }                                                                                  \
+  } while (0)
+__device__ __forceinline__ unsigned long long attn_gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  if (pipe < kTrPipes && k < kTrEvents / 4) g_attn_trace[pipe * kTrEvents + role * (kTrEvents / 4) + k] = (t << 8) | code;
-  ++k;
+  return t;
 }
-#define ATR(role, code) attn_tr(2 * static_cast<int>(blockIdx.x) + pp, role, code, tr_k)
-#define ATR_DONE(role) \
-  do { if (2 * static_cast<int>(blockIdx.x) + pp < kTrPipes) g_attn_trace_n[(2 * blockIdx.x + pp) * 4 + (role)] = tr_k; } while (0)
-extern "C" int elis_debug_attn_trace(unsigned long long* host, unsigned* counts, int reset) {
-  if (reset) {
-    void* p = nullptr;
-    cudaGetSymbolAddress(&p, g_attn_trace_n);
-    return static_cast<int>(cudaMemset(p, 0, sizeof(g_attn_trace_n)));
-  }
-  cudaError_t e = cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(g_attn_trace));
-  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(counts, g_attn_trace_n, sizeof(g_attn_trace_n));
-  return static_cast<int>(e);
+__device__ __forceinline__ unsigned attn_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
 }
 #else
-#define ATR(role, code) do { } while (0)
-#define ATR_DONE(role) do { } while (0)
+#define ATTN_TRACE(slot, val) \
+  do {                        \
+  } while (0)
 #endif
 
 namespace {
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ 
   const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
   if (item >= __ldg(num_work)) return;
   const AttnWork w = work[item];
-  const int start = w.start[0], L = w.len[0], q0 = w.q0;
+  const int start = w.start, L = w.len, q0 = w.q0;
   const int ld = 3 * H;
   const uint16_t* gQ = qkv + static_cast<size_t>(start) * ld + h * D;
   const uint16_t* gK = gQ + H;
@@ -226,47 +226,30 @@ __global__ void __launch_bounds__(128) k_attention(const uint16_t* __restrict__ 
   }
 }
 // ============================================================================ tcgen05 engine
-// Persistent, warp-specialised; one CTA per SM running two independent pipelines, each:
-//   TMA warp   producer: a work item's Q rows (double-buffered slot) and its K and V key blocks
-//              (2-stage rings each) as 32-row boxes from the head-major qkv planes the QKV GEMM
-//              writes ([3 nh][T][64]: plane h = Q of head h, nh + h = K, 2 nh + h = V);
-//   MMA warp   issuer (one thread), in the order S_0, S_1, PV_0, S_2, PV_1, ... over the
-//              pipeline's blocks (across items):  S_g = Q K_g^T (tcgen05 M 128 x N 128 x K 64,
-//              TMEM columns [0, 128)) as soon as the softmax has read S_{g-1} into registers;
-//              O += P_g V_g (A = P_g from TMEM columns [128, 192), B = V_g MN-major from shared
-//              memory, accumulator in columns [192, 256)) once the softmax has written P_g;
-//   4 warps    softmax + epilogue, thread = query row = TMEM lane: a block's scores are read once
-//              into registers (then S is released to the next block's MMA), block max, exp2 (part
-//              on the FMA pipe), row sum, P packed to 16 bits into the P columns once the previous
-//              PV has read them; O stays in TMEM across key blocks and is rescaled only when the
-//              running max grows by more than 2^8 (lazy rescale: P <= 256); after the last block
-//              ctx = O / l is staged in the item's Q slot and written back 4 rows per instruction.
-// So the next block's S (and the next item's first S) is computed while the softmax of the
-// current one runs, and the loads run up to two blocks ahead; the other pipeline overlaps its own
-// chain with this one (TMEM 2 x 256 columns, shared memory 2 x 96 KB).  Registers: the launch
-// gives 168 per thread; setmaxnreg moves them from the control warpgroup (40) to the two softmax
-// warpgroups (232 each: a block's 128 scores per row held in registers).
-// Short requests (<= 128 tokens) arrive packed (AttnWork): request k owns 32-row segments
-// [f_k, f_k + ceil(L_k / 32)) of the tile -- one softmax warp per segment -- and attends only to
-// its own key segments (block-diagonal mask; P is zero elsewhere), so a request costs
-// ceil(L / 32) x 32 rows instead of a 128-row tile.  Its arithmetic is independent of f_k: the
-// same 32-key chunks in the same order, the PV MMA's 16-key steps hold keys of one request only
-// and the other steps add exact zeros (batch invariance).
-constexpr int TQ = 128;        // q rows per tile (= TMEM lanes)
-constexpr int TKB = 128;       // keys per block
+// One CTA (4 warps) = (request, head, 128-row q tile), head dim 64; thread = query row = TMEM
+// lane.  Q, K, V come from the head-major qkv planes the QKV GEMM writes ([3 nh][T][64]), so
+// every TMA box is one contiguous 16 KB block.  Keys are processed in blocks of 128 (<= 4 per
+// request, BERT max 512 tokens):
+//   S_j = Q K_j^T        tcgen05 M 128 x N 128 x K 64, into TMEM columns [0, 128)
+//   softmax block j      2 passes over the TMEM row (block max, then exp2 / sum), online
+//                        rescaling of (m, l, O) with fp32 statistics; P_j packed to bf16
+//                        pairs into TMEM columns [0, 64) over consumed scores
+//   O_j = P_j V_j        tcgen05 with A = P_j from TMEM, B = V_j (MN-major) from shared memory,
+//                        into TMEM columns [64, 128); accumulated in registers as O = a O + O_j
+//   ctx = O / l          bf16
+// Thread 0 issues the TMA loads (K_{j+1} overlaps softmax j, V_{j+1} overlaps S_{j+1}) and
+// the MMAs in program order.  128 TMEM columns, 48 KB of shared memory and <= 128 registers
+// per thread let 4 CTAs share an SM, so one CTA's loads and MMAs overlap another's softmax.
+// (A persistent warp-specialised variant -- producer / MMA / softmax warps, 2 CTAs per SM --
+// measured slower: 2.17 vs 1.75 ms per BGE-base step; see git history.)
+// Keys >= L (the next request's) are masked; 32-key chunks / 16-key MMA steps with no valid
+// key and query warps whose rows all lie beyond L are skipped.
+constexpr int TQ = 128;        // q rows per CTA (= TMEM lanes)
+constexpr int TKB = 128;       // keys per K/V block
 constexpr int TD = 64;         // head dim
-constexpr int kBoxRows = 32;   // TMA box: 32 rows x 64 columns (one 128-byte SWIZZLE_128B row each)
-constexpr int kBoxBytes = kBoxRows * TD * 2;  // 4 KB
-constexpr int kBlkBytes = TKB * TD * 2;       // 16 KB
-constexpr int kAwsKV = 2;                     // K/V ring stages (K + V per stage)
-// warps 0-3: TMA producer / MMA issuer of pipelines 0 and 1; warps 4-7 / 8-11: softmax of pipeline 0 / 1
-constexpr int kAwsThreads = 384;
-constexpr uint32_t kAwsRegsCtl = 40, kAwsRegsSoftmax = 232;  // 128 x 40 + 256 x 232 = 384 x 168 registers
-constexpr int kPipeSmem = 2 * kBlkBytes + kAwsKV * 2 * kBlkBytes;  // Q slots + K and V rings: 96 KB
-constexpr int kAttnTcSmem = 2 * kPipeSmem + 1024 + 512;
-constexpr uint32_t kPCol = 128;               // P (16-bit pairs): TMEM columns [128, 192)
-constexpr uint32_t kOCol = 192;               // O accumulator: TMEM columns [192, 256)
-constexpr float kLazyRescale = 8.f;           // log2 units
+constexpr int kBlkBytes = TKB * TD * 2;  // 16 KB
+constexpr int kAttnTcSmem = 3 * kBlkBytes + 1024 + 256;
+constexpr uint32_t kOCol = 64;
 // packed fp32 pairs (Blackwell FFMA2 / FADD2: two lanes of fp32 math per instruction)
 ELIS_DEV unsigned long long f2_pack(float lo, float hi) {
   unsigned long long r;
@@ -286,11 +269,6 @@ ELIS_DEV unsigned long long f2_add(unsigned long long a, unsigned long long b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-ELIS_DEV unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 ELIS_DEV float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -302,12 +280,12 @@ ELIS_DEV float ex2_approx(float x) {
   return r;
 }
 // exp2 of a pair on the FMA pipe, to take part of the softmax exponentials off the MUFU
-// (16 ex2 / clk / SM, measured: scripts/tmem_bw.cu):
+// (16 ex2 / clk / SM, the softmax bound when 4 CTAs share an SM):
 //   j = rint(x) (x + 1.5 * 2^23 leaves j in the low mantissa bits), f = x - j in [-1/2, 1/2],
 //   2^f = degree-3 minimax polynomial (max relative error 7.5e-5, scripts/fit_exp2.py; P is then
-//   rounded to 16 bits), 2^x = bits(2^f) + (j << 23).
+//   rounded to bf16, relative step 3.9e-3), 2^x = bits(2^f) + (j << 23).
 // x is clamped at -125 so the exponent stays normal (the true value is then < 2^-125 next to the
-// row maximum's >= 1).
+// row maximum's 1).
 #ifndef ELIS_EXP2_POLY
 #define ELIS_EXP2_POLY 6  // pairs of every 16 in a 32-key chunk evaluated by exp2_poly2
 #endif
@@ -329,513 +307,260 @@ ELIS_DEV constexpr bool exp2_on_fma(int pair) {
   return ((pair + 1) * ELIS_EXP2_POLY) / 16 != (pair * ELIS_EXP2_POLY) / 16;  // spread over the chunk
 }
 
-ELIS_DEV AttnWork load_work(const AttnWork* w) {
-  const int4 a = __ldg(reinterpret_cast<const int4*>(w));
-  const int4 b = __ldg(reinterpret_cast<const int4*>(w) + 1);
-  AttnWork r;
-  *reinterpret_cast<int4*>(&r) = a;
-  *(reinterpret_cast<int4*>(&r) + 1) = b;
-  return r;
-}
-ELIS_DEV bool tile_packed(const AttnWork& w) { return w.len[0] <= TKB; }
-ELIS_DEV int tile_nkb(const AttnWork& w) { return tile_packed(w) ? 1 : (w.len[0] + TKB - 1) / TKB; }
-ELIS_DEV int ceil32(int x) { return (x + 31) >> 5; }
-// keys of block j the PV product runs over (the last request's end, for a packed tile)
-ELIS_DEV int tile_key_hi(const AttnWork& w, int j) {
-  if (!tile_packed(w)) return min(TKB, w.len[0] - TKB * j);
-  int f = 0, hi = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (k < w.nreq) { hi = 32 * f + w.len[k]; f += ceil32(w.len[k]); }
-  return hi;
-}
-// one softmax warp's share of a tile: query rows 32 q .. 32 q + 31 of the tile
-struct WarpRows {
-  bool active;
-  int tok;    // token of row 32 q
-  int rows;   // valid rows (1..32)
-  int ch0;    // first key chunk (32 keys) of the warp's keys within a block
-  int klen;   // packed: the request's length (its keys); long: the request length L
-};
-ELIS_DEV WarpRows warp_rows(const AttnWork& w, int q) {
-  WarpRows r{false, 0, 0, 0, 0};
-  if (tile_packed(w)) {
-    int f = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < w.nreq) {
-        const int sg = ceil32(w.len[k]);
-        if (q >= f && q < f + sg) {
-          r.active = true;
-          r.tok = w.start[k] + 32 * (q - f);
-          r.rows = min(32, w.len[k] - 32 * (q - f));
-          r.ch0 = f;
-          r.klen = w.len[k];
-        }
-        f += sg;
-      }
-    }
-  } else {
-    const int L = w.len[0], q0 = w.q0 + 32 * q;
-    r.active = q0 < L;
-    r.tok = w.start[0] + q0;
-    r.rows = min(32, L - q0);
-    r.ch0 = 0;
-    r.klen = L;
-  }
-  return r;
-}
-
-// One key block's softmax for one warp's 32 rows (thread = row), NCH = 32-key chunks holding the
-// row's nk valid keys from chunk ch0 of the block; straight-line code per NCH.  S is read once into
-// registers, then `release` (the S columns may be overwritten by the next S MMA) runs; block max;
-// lazy running max (j > 0: it moves only when the block's exceeds it by more than 2^8);
-// p = exp2(s scale - m) (part on the FMA pipe); row sum in a fixed order; then `before_p` (the
-// previous PV has read the P columns; O rescaled if needed) runs and P is packed to 16 bits into
-// the P columns (chunk c at 16 (ch0 + c)).  Returns the block's row sum.
-template <int NCH, bool F16, class Release, class BeforeP>
-ELIS_DEV float softmax_block(uint32_t taddr, int ch0, int nk, int j, float scale_log2, float& m, bool& resc,
-                             float& alpha, Release&& release, BeforeP&& before_p) {
-  uint32_t r[NCH][32];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) tmem_ld_32x32b_x32(taddr + (ch0 + c) * 32, r[c]);
-  tc_wait_ld();
-  release();
-  const int tail = nk - 32 * (NCH - 1);  // valid keys of the last chunk (1..32)
-  if (tail < 32) {
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (e >= tail) r[NCH - 1][e] = __float_as_uint(-INFINITY);
-  }
-  float mx[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(r[0][i]);
-#pragma unroll
-  for (int c = 0; c < NCH; ++c)
-#pragma unroll
-    for (int e = (c == 0 ? 8 : 0); e < 32; e += 2) {
-      const int i = (e >> 1) & 7;
-      mx[i] = fmax3(mx[i], __uint_as_float(r[c][e]), __uint_as_float(r[c][e + 1]));
-    }
-  const float bm = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
-  const float ms = bm * scale_log2;  // finite: every block has >= 1 valid key
-  alpha = 1.f;
-  resc = false;
-  if (j == 0) {
-    m = ms;
-  } else if (ms > m + kLazyRescale) {
-    alpha = ex2_approx(m - ms);
-    m = ms;
-    resc = true;
-  }
-  const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
-  const unsigned long long nm2 = f2_pack(-m, -m);
-#pragma unroll
-  for (int e = 0; e < 16; ++e) {
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      float x0, x1, p0, p1;
-      f2_unpack(f2_fma(f2_pack(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1])), sc2, nm2), x0, x1);
-      if (exp2_on_fma(e)) {
-        f2_unpack(exp2_poly2(x0, x1), p0, p1);
-      } else {
-        p0 = ex2_approx(x0);
-        p1 = ex2_approx(x1);
-      }
-      r[c][2 * e] = __float_as_uint(p0);
-      r[c][2 * e + 1] = __float_as_uint(p1);
-    }
-  }
-  float bsum = 0.f;
-  uint32_t pk[NCH][16];
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    unsigned long long a0 = f2_pack(__uint_as_float(r[c][0]), __uint_as_float(r[c][1]));
-    unsigned long long a1 = f2_pack(__uint_as_float(r[c][2]), __uint_as_float(r[c][3]));
-    unsigned long long a2 = f2_pack(__uint_as_float(r[c][4]), __uint_as_float(r[c][5]));
-    unsigned long long a3 = f2_pack(__uint_as_float(r[c][6]), __uint_as_float(r[c][7]));
-#pragma unroll
-    for (int e = 8; e < 32; e += 8) {
-      a0 = f2_add(a0, f2_pack(__uint_as_float(r[c][e]), __uint_as_float(r[c][e + 1])));
-      a1 = f2_add(a1, f2_pack(__uint_as_float(r[c][e + 2]), __uint_as_float(r[c][e + 3])));
-      a2 = f2_add(a2, f2_pack(__uint_as_float(r[c][e + 4]), __uint_as_float(r[c][e + 5])));
-      a3 = f2_add(a3, f2_pack(__uint_as_float(r[c][e + 6]), __uint_as_float(r[c][e + 7])));
-    }
-    float s0, s1, s2, s3;
-    f2_unpack(f2_add(a0, a1), s0, s1);
-    f2_unpack(f2_add(a2, a3), s2, s3);
-    bsum += (s0 + s1) + (s2 + s3);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) pk[c][e] = pack16x2<F16>(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]));
-  }
-  before_p();
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) tmem_st_32x32b_x16(taddr + kPCol + (ch0 + c) * 16, pk[c]);
-  return bsum;
-}
-
 // F8OUT: ctx written as E4M3(ctx_scale * ctx) bytes [T, H] (the FP8 out-projection's A operand)
 // F16: Q, K, V, P and ctx in fp16 instead of bf16 (fp16 operand precision)
 template <bool F8OUT, bool F16>
-__global__ void __launch_bounds__(kAwsThreads, 1)
-    k_attention_tc(const __grid_constant__ CUtensorMap tm, const AttnWork* __restrict__ work,
-                   const int32_t* __restrict__ num_work, int H, int nh, uint16_t* __restrict__ ctx,
-                   float scale_log2, int Tp, float ctx_scale) {
+__global__ void __launch_bounds__(128, 4)
+    k_attention_tc(const __grid_constant__ CUtensorMap tm,
+                   const AttnWork* __restrict__ work, const int32_t* __restrict__ num_work, int H, int nh,
+                   uint16_t* __restrict__ ctx, float scale_log2, int Tp, float ctx_scale) {
+#ifdef ELIS_ATTN_TRACE
+  const unsigned long long t_start = attn_gtime();
+#endif
+  // the work entry is read together with num_work (the list has capacity for every CTA; entries
+  // past num_work are never used) and carries the request bounds: no dependent loads
+  const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
+  const AttnWork w = work[item];
+  if (item >= __ldg(num_work)) return;
+  ATTN_TRACE(0, t_start);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  const int warp = warp_id(), lane = lane_id();
-  // pipeline of this warp: control warps 2 pp (TMA) / 2 pp + 1 (MMA), softmax warps 4 + 4 pp .. 7 + 4 pp
-  const int pp = warp < 4 ? warp >> 1 : (warp - 4) >> 2;
-  uint8_t* sQ = smem + pp * kPipeSmem;                 // [2][16 KB]
-  uint8_t* sK = sQ + 2 * kBlkBytes;                    // [kAwsKV][16 KB]
-  uint8_t* sV = sK + kAwsKV * kBlkBytes;               // [kAwsKV][16 KB]
-  uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + 2 * kPipeSmem);
-  constexpr int kBarsPerPipe = 24;
-  uint64_t* bars = bars_all + pp * kBarsPerPipe;
-  uint64_t* q_full = bars;                  // [2]  Q slot loaded (TMA bytes)
-  uint64_t* q_empty = bars + 2;             // [2]  Q slot free (4 softmax warps, after the epilogue)
-  uint64_t* k_full = bars + 4;              // [kAwsKV]
-  uint64_t* k_empty = bars + 6;             // [kAwsKV]  (commit: S_g done)
-  uint64_t* v_full = bars + 8;              // [kAwsKV]
-  uint64_t* v_empty = bars + 10;            // [kAwsKV]  (commit: PV_g done)
-  uint64_t* s_full = bars + 12;             // S_g in TMEM (commit)
-  uint64_t* s_free = bars + 13;             // S_g read into registers (4 softmax warps)
-  uint64_t* p_full = bars + 14;             // P_g in TMEM (4 softmax warps)
-  uint64_t* p_free = bars + 15;             // PV_g done: P columns free, O stable (commit)
-  uint64_t* o_full = bars + 16;             // the item's last PV done (commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars_all + 2 * kBarsPerPipe);
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kBlkBytes;
+  uint8_t* sV = sK + kBlkBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kBlkBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = bars + 2;
+  uint64_t* s_full = bars + 3;
+  uint64_t* o_full = bars + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
 
-  const int nitems = __ldg(num_work) * nh;
-  const int G = 2 * static_cast<int>(gridDim.x);       // pipelines in the grid
-  const int first = 2 * static_cast<int>(blockIdx.x) + pp;
-  if (warp == 0 && lane == 0) {
+  const int start = w.start, L = w.len, q0 = w.q0;
+  const int nkb = (L + TKB - 1) / TKB;  // 1..4
+  const int warp = warp_id(), lane = lane_id();
+  const bool issuer = threadIdx.x == 0;
+
+  if (issuer) {  // barriers + the first loads go out before the TMEM allocation / CTA barrier
     tma_prefetch_desc(&tm);
-    for (int x = 0; x < 2; ++x) {
-      uint64_t* b = bars_all + x * kBarsPerPipe;
-      for (int i = 0; i < 2; ++i) {
-        mbar_init(&b[i], 1);
-        mbar_init(&b[2 + i], 4);
-        mbar_init(&b[4 + i], 1);
-        mbar_init(&b[6 + i], 1);
-        mbar_init(&b[8 + i], 1);
-        mbar_init(&b[10 + i], 1);
-      }
-      mbar_init(&b[12], 1);
-      mbar_init(&b[13], 4);
-      mbar_init(&b[14], 4);
-      mbar_init(&b[15], 1);
-      mbar_init(&b[16], 1);
-    }
+    mbar_init(q_full, 1);
+    mbar_init(k_full, 1);
+    mbar_init(v_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(o_full, 1);
     fence_mbar_init();
+    mbar_arrive_expect_tx(q_full, kBlkBytes);
+    tma_load_2d(sQ, &tm, q_full, 0, h * Tp + start + q0);
+    mbar_arrive_expect_tx(k_full, kBlkBytes);
+    tma_load_2d(sK, &tm, k_full, 0, (nh + h) * Tp + start);
+    mbar_arrive_expect_tx(v_full, kBlkBytes);
+    tma_load_2d(sV, &tm, v_full, 0, (2 * nh + h) * Tp + start);
   }
-  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<128>(tmem_slot);  // warp 0's thread 0 is issuing the loads
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot + pp * 256;   // this pipeline's S [0,128), P [128,192), O [192,256)
+  const uint32_t tmem = *tmem_slot;
+  ATTN_TRACE(1, attn_gtime());
+  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int row = warp * 32 + lane;
+  // warps whose 32 query rows all lie beyond L skip the softmax (their rows are never stored;
+  // MMA rows are independent)
+  const bool warp_active = q0 + warp * 32 < L;
 
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kAwsRegsCtl));
-    if ((warp & 1) == 0 && lane == 0) {
-      // ---------------- TMA producer: the 32-row boxes of the tile's Q and of each key block; box s
-      // of the tile's request k (packed) lands in slot f_k + s, a long request's rows in slots 0..
-      uint32_t kvn = 0, itn = 0;
-      unsigned tr_k = 0;
-      (void)tr_k;
-      for (int item = first; item < nitems; item += G, ++itn) {
-        const AttnWork w = load_work(work + item / nh);
-        const int h = item % nh;
-        const int qs = itn & 1;
-        const bool packed = tile_packed(w);
-        ATR(0, 1);
-        mbar_wait(&q_empty[qs], ((itn >> 1) & 1) ^ 1u);
-        ATR(0, 2);
-        uint8_t* dq = sQ + qs * kBlkBytes;
-        int nbq = 0;
-        if (packed) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) nbq += k < w.nreq ? ceil32(w.len[k]) : 0;
-        } else {
-          nbq = ceil32(min(TKB, w.len[0] - w.q0));
-        }
-        mbar_arrive_expect_tx(&q_full[qs], nbq * kBoxBytes);
-        if (packed) {
-          int f = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (k < w.nreq) {
-              const int sg = ceil32(w.len[k]);
-              for (int x = 0; x < sg; ++x)
-                tma_load_2d(dq + (f + x) * kBoxBytes, &tm, &q_full[qs], 0, h * Tp + w.start[k] + 32 * x);
-              f += sg;
-            }
-          }
-        } else {
-          for (int x = 0; x < nbq; ++x)
-            tma_load_2d(dq + x * kBoxBytes, &tm, &q_full[qs], 0, h * Tp + w.start[0] + w.q0 + 32 * x);
-        }
-        const int nkb = tile_nkb(w);
-        for (int j = 0; j < nkb; ++j, ++kvn) {
-          const int s = kvn % kAwsKV;
-          const uint32_t par = ((kvn / kAwsKV) & 1) ^ 1u;
-          const int nb = packed ? nbq : ceil32(min(TKB, w.len[0] - TKB * j));  // packed: Q's boxes
-          for (int kv = 0; kv < 2; ++kv) {  // K_j, then V_j (each ring frees at its own MMA)
-            uint64_t* fullb = kv ? &v_full[s] : &k_full[s];
-            ATR(0, 3);
-            mbar_wait(kv ? &v_empty[s] : &k_empty[s], par);
-            ATR(0, 4);
-            mbar_arrive_expect_tx(fullb, nb * kBoxBytes);
-            uint8_t* dst = (kv ? sV : sK) + s * kBlkBytes;
-            const int rowp = (kv ? 2 * nh + h : nh + h) * Tp;
-            if (packed) {
-              int f = 0;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (k < w.nreq) {
-                  const int sg = ceil32(w.len[k]);
-                  for (int x = 0; x < sg; ++x)
-                    tma_load_2d(dst + (f + x) * kBoxBytes, &tm, fullb, 0, rowp + w.start[k] + 32 * x);
-                  f += sg;
-                }
-              }
-            } else {
-              const int t0 = w.start[0] + TKB * j;
-              for (int x = 0; x < nb; ++x) tma_load_2d(dst + x * kBoxBytes, &tm, fullb, 0, rowp + t0 + 32 * x);
-            }
-          }
-        }
-      }
-      ATR_DONE(0);
-    } else if ((warp & 1) == 1 && lane == 0) {
-      // ---------------- MMA issuer: S_0, S_1, PV_0, S_2, PV_1, ... over the pipeline's blocks
-      constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB) : make_idesc_bf16_f32(TQ, TKB);
-      constexpr uint32_t idesc_o =
-          (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);  // V MN-major
-      unsigned tr_k = 0;
-      (void)tr_k;
-      // S cursor (ahead) and PV cursor (one block behind), each (item, block, global block, item count)
-      int s_item = first, s_j = 0, p_item = first, p_j = 0;
-      uint32_t s_g = 0, s_itn = 0, p_g = 0;
-      AttnWork s_w{}, p_w{};
-      if (s_item < nitems) s_w = load_work(work + s_item / nh);
-      p_w = s_w;
-      auto issue_s = [&]() {  // S of the S cursor's block; advances the cursor
-        const int qs = s_itn & 1;
-        if (s_j == 0) {
-          ATR(1, 10);
-          mbar_wait(&q_full[qs], (s_itn >> 1) & 1);
-          ATR(1, 11);
-        }
-        const int s = s_g % kAwsKV;
-        ATR(1, 12);
-        mbar_wait(&k_full[s], (s_g / kAwsKV) & 1);
-        if (s_g > 0) mbar_wait(s_free, (s_g - 1) & 1);  // the softmax has read S_{g-1}
-        ATR(1, 13);
-        tc_fence_after();
-        const uint64_t dq = make_sw128_desc(smem_u32(sQ + qs * kBlkBytes));
-        const uint64_t dk = make_sw128_desc(smem_u32(sK + s * kBlkBytes));
-#pragma unroll
-        for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
-        tc_commit(s_full);
-        tc_commit(&k_empty[s]);
-        ++s_g;
-        if (++s_j == tile_nkb(s_w)) {
-          s_j = 0;
-          ++s_itn;
-          s_item += G;
-          if (s_item < nitems) s_w = load_work(work + s_item / nh);
-        }
-      };
-      if (s_item < nitems) issue_s();
-      while (p_item < nitems) {
-        // within an item S_{g+1} goes before PV_g (the softmax of block g + 1 overlaps PV_g); the
-        // next item's first S after the item's last PV (its Q / K may still be loading)
-        if (s_item == p_item) issue_s();
-        const int s = p_g % kAwsKV;
-        ATR(1, 14);
-        mbar_wait(p_full, p_g & 1);
-        mbar_wait(&v_full[s], (p_g / kAwsKV) & 1);
-        ATR(1, 15);
-        tc_fence_after();
-        const int nks = (tile_key_hi(p_w, p_j) + 15) / 16;  // 16-key steps holding keys of the tile
-        const uint8_t* sv = sV + s * kBlkBytes;
-        for (int ks = 0; ks < nks; ++ks) {
-          const uint64_t dv = make_sw128_desc(smem_u32(sv + ks * (16 * TD * 2)));
-          tc_mma_f16_tmem_a(tmem + kOCol, tmem + kPCol + ks * 8, dv, idesc_o, (p_j | ks) != 0 ? 1u : 0u);
-        }
-        tc_commit(&v_empty[s]);
-        tc_commit(p_free);
-        ++p_g;
-        if (++p_j == tile_nkb(p_w)) {
-          tc_commit(o_full);
-          p_j = 0;
-          p_item += G;
-          if (p_item < nitems) p_w = load_work(work + p_item / nh);
-          if (s_item < nitems && s_item == p_item) issue_s();  // the next item's first S
-        }
-      }
-      ATR_DONE(1);
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kAwsRegsSoftmax));
-    // ---------------- softmax + epilogue (TMEM lane quarter q = warp & 3)
-    const int q = warp & 3;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const int row = q * 32 + lane;
-    uint32_t g = 0, itn = 0;
-    unsigned tr_k = 0;
-    (void)tr_k;
-    AttnWork wn = load_work(work + min(first, max(nitems - 1, 0)) / nh);  // prefetched work entry
-    for (int item = first; item < nitems; item += G, ++itn) {
-      const AttnWork w = wn;
-      if (item + G < nitems) wn = load_work(work + (item + G) / nh);
-      const int h = item % nh;
-      const int nkb = tile_nkb(w);
-      const WarpRows wr = warp_rows(w, q);
-      const bool packed = tile_packed(w);
-      // packed tiles: P is zero outside the warp's own key chunks within [0, tile_nch)
-      const int tile_nch = packed ? ceil32(tile_key_hi(w, 0)) : 0;
-      float m = 0.f, l = 0.f;  // running row max (scaled, log2 domain) and row sum
-      for (int j = 0; j < nkb; ++j, ++g) {
-        if (q == 0 && lane == 0) ATR(2, 20);
-        mbar_wait(s_full, g & 1);
-        if (q == 0 && lane == 0) ATR(2, 21);
-        tc_fence_after();
-        auto release = [&]() {  // S_g is in registers: the next S may overwrite the columns
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_free);
-        };
-        if (wr.active) {
-          const int nk = packed ? wr.klen : min(TKB, wr.klen - TKB * j);  // valid keys of this block
-          const int nch = ceil32(nk);
-          float alpha = 1.f;
-          bool resc = false;
-          auto before_p = [&]() {  // PV_{g-1} has read the P columns and O is complete
-            if (g > 0) mbar_wait(p_free, (g - 1) & 1);
-            tc_fence_after();
-            if (resc) {  // O *= alpha
-              const unsigned long long al2 = f2_pack(alpha, alpha);
-#pragma unroll
-              for (int x = 0; x < 2; ++x) {
-                uint32_t o[32];
-                tmem_ld_32x32b_x32(taddr + kOCol + x * 32, o);
-                tc_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  float o0, o1;
-                  f2_unpack(f2_mul(f2_pack(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])), al2), o0, o1);
-                  o[2 * i] = __float_as_uint(o0);
-                  o[2 * i + 1] = __float_as_uint(o1);
-                }
-                tmem_st_32x32b_x32(taddr + kOCol + x * 32, o);
-              }
-            }
-            if (packed) {  // other requests' key chunks of the tile: P = 0
-              uint32_t z[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) z[e] = 0u;
-              for (int c = 0; c < tile_nch; ++c)
-                if (c < wr.ch0 || c >= wr.ch0 + nch) tmem_st_32x32b_x16(taddr + kPCol + c * 16, z);
-            }
-          };
-          float bsum;
-          switch (nch) {
-            case 1: bsum = softmax_block<1, F16>(taddr, wr.ch0, nk, j, scale_log2, m, resc, alpha, release, before_p); break;
-            case 2: bsum = softmax_block<2, F16>(taddr, wr.ch0, nk, j, scale_log2, m, resc, alpha, release, before_p); break;
-            case 3: bsum = softmax_block<3, F16>(taddr, wr.ch0, nk, j, scale_log2, m, resc, alpha, release, before_p); break;
-            default: bsum = softmax_block<4, F16>(taddr, wr.ch0, nk, j, scale_log2, m, resc, alpha, release, before_p); break;
-          }
-          l = (j == 0) ? bsum : (resc ? l * alpha : l) + bsum;
-          tc_wait_st();
-        } else {
-          release();
-          // no P to write, but p_full(g) must not be arrived before phase g - 1 completed: an early
-          // second arrival would count toward the wrong phase
-          if (g > 0) mbar_wait(p_free, (g - 1) & 1);
-        }
-        if (q == 0 && lane == 0) ATR(2, 28);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
-        if (q == 0 && lane == 0) ATR(2, 22);
-      }
-      // ---- epilogue: ctx = O / l, staged in this item's Q slot (every S MMA of the item is complete
-      // once o_full fires), rows XOR-swizzled in 16-byte pieces, then 4 rows per warp instruction
-      if (q == 0 && lane == 0) ATR(2, 23);
-      mbar_wait(o_full, itn & 1);
-      if (q == 0 && lane == 0) ATR(2, 24);
+  constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB) : make_idesc_bf16_f32(TQ, TKB);
+  constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);  // V MN-major
+  if (issuer) mbar_wait(q_full, 0);
+  float m = -INFINITY, l = 0.f;   // running row max (scaled, log2 domain) and row sum
+  unsigned long long o2[TD / 2];  // O as fp32 pairs
+  const unsigned long long zero2 = f2_pack(0.f, 0.f);
+
+  for (int j = 0; j < nkb; ++j) {
+    const uint32_t ph = j & 1;
+    if (issuer) {
+      // S_j = Q K_j^T (4 x K16 steps, +32 B inside the 128 B swizzle row)
+      mbar_wait(k_full, ph);
       tc_fence_after();
-      const int qs = itn & 1;
-      uint8_t* stg = sQ + qs * kBlkBytes;
-      if (wr.active) {
+      const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+      const uint64_t dk = make_sw128_desc(smem_u32(sK));
 #pragma unroll
-        for (int x = 0; x < 2; ++x) {  // one 32-column half of O at a time
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(taddr + kOCol + x * 32, v);
-          tc_wait_ld();
-          if constexpr (F8OUT) {  // 64-byte rows: 4 pieces, XOR-swizzled by row & 3
-            const float inv = ctx_scale / l;
-            uint4* srow = reinterpret_cast<uint4*>(stg + row * TD);
+      for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+      tc_commit(s_full);
+    }
+    mbar_wait(s_full, ph);
+    tc_fence_after();
+    if (j == 0) ATTN_TRACE(2, attn_gtime());
+    if (issuer && j + 1 < nkb) {  // the S MMA has consumed K_j: prefetch K_{j+1}
+      mbar_arrive_expect_tx(k_full, kBlkBytes);
+      tma_load_2d(sK, &tm, k_full, 0, (nh + h) * Tp + start + (j + 1) * TKB);
+    }
+    const int nvalid_blk = L - j * TKB;  // keys >= L belong to other requests: masked
+    // 32-key chunks holding valid keys
+    const int nch = warp_active ? min(TKB / 32, (nvalid_blk + 31) / 32) : 0;
+    // pass A: block max (single-buffered TMEM loads: registers are budgeted for 4 CTAs / SM).
+    // Only the chunk holding the last valid key is masked.
+    uint32_t r[32];
+    float bm = -INFINITY;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const uint32_t* u = v + 16 * k;
-              srow[(2 * x + k) ^ (row & 3)] = make_uint4(
-                  pack_e4m3x4(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv, __uint_as_float(u[2]) * inv,
-                              __uint_as_float(u[3]) * inv),
-                  pack_e4m3x4(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv, __uint_as_float(u[6]) * inv,
-                              __uint_as_float(u[7]) * inv),
-                  pack_e4m3x4(__uint_as_float(u[8]) * inv, __uint_as_float(u[9]) * inv, __uint_as_float(u[10]) * inv,
-                              __uint_as_float(u[11]) * inv),
-                  pack_e4m3x4(__uint_as_float(u[12]) * inv, __uint_as_float(u[13]) * inv, __uint_as_float(u[14]) * inv,
-                              __uint_as_float(u[15]) * inv));
-            }
+    for (int c = 0; c < TKB / 32; ++c) {
+      if (c < nch) {
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tc_wait_ld();
+        const int nv = nvalid_blk - c * 32;
+        if (nv < 32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e >= nv) r[e] = __float_as_uint(-INFINITY);
+        }
+        float t[11];
+#pragma unroll
+        for (int e = 0; e < 10; ++e)
+          t[e] = fmax3(__uint_as_float(r[3 * e]), __uint_as_float(r[3 * e + 1]), __uint_as_float(r[3 * e + 2]));
+        t[10] = fmax3(__uint_as_float(r[30]), __uint_as_float(r[31]), bm);
+        bm = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmax3(t[6], t[7], fmax3(t[8], t[9], t[10])));
+      }
+    }
+    const float m_new = fmaxf(m, bm * scale_log2);  // finite: every block has >= 1 valid key
+    const float alpha = ex2_approx(m - m_new);      // 0 on the first block
+    m = m_new;
+    // pass B: p = exp2(s*scale - m), block sum, P (bf16 pairs) over consumed score columns
+    const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
+    const unsigned long long nm2 = f2_pack(-m, -m);
+    unsigned long long acc0 = zero2, acc1 = zero2;  // 2 x 2 independent partial sums, fixed order
+#pragma unroll
+    for (int c = 0; c < TKB / 32; ++c) {
+      if (c < nch) {
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tc_wait_ld();
+        const int nv = nvalid_blk - c * 32;
+        float p[32];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float x0, x1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])), sc2, nm2), x0, x1);
+          if (exp2_on_fma(e)) {
+            f2_unpack(exp2_poly2(x0, x1), p[2 * e], p[2 * e + 1]);
           } else {
-            const float inv = 1.0f / l;
-            uint4* srow = reinterpret_cast<uint4*>(stg + row * (TD * 2));
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t* u = v + 8 * k;
-              srow[(4 * x + k) ^ (row & 7)] =
-                  make_uint4(pack16x2<F16>(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv),
-                             pack16x2<F16>(__uint_as_float(u[2]) * inv, __uint_as_float(u[3]) * inv),
-                             pack16x2<F16>(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv),
-                             pack16x2<F16>(__uint_as_float(u[6]) * inv, __uint_as_float(u[7]) * inv));
-            }
+            p[2 * e] = ex2_approx(x0);
+            p[2 * e + 1] = ex2_approx(x1);
           }
         }
-        __syncwarp();
-        if constexpr (F8OUT) {
-          uint8_t* c8 = reinterpret_cast<uint8_t*>(ctx);
-          const int c = lane & 3;
-          for (int rr = lane >> 2; rr < wr.rows; rr += 8) {
-            const int sr = q * 32 + rr;
-            const uint4 val = reinterpret_cast<const uint4*>(stg + sr * TD)[c ^ (sr & 3)];
-            *reinterpret_cast<uint4*>(c8 + static_cast<size_t>(wr.tok + rr) * H + h * TD + c * 16) = val;
-          }
-        } else {
-          const int c = lane & 7;
-          for (int rr = lane >> 3; rr < wr.rows; rr += 4) {
-            const int sr = q * 32 + rr;
-            const uint4 val = reinterpret_cast<const uint4*>(stg + sr * (TD * 2))[c ^ (sr & 7)];
-            *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(wr.tok + rr) * H + h * TD + c * 8) = val;
-          }
+        if (nv < 32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) p[e] = (e < nv) ? p[e] : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc0 = f2_add(acc0, f2_pack(p[4 * e], p[4 * e + 1]));
+          acc1 = f2_add(acc1, f2_pack(p[4 * e + 2], p[4 * e + 3]));
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = pack16x2<F16>(p[2 * e], p[2 * e + 1]);
+        tmem_st_32x32b_x16(taddr + c * 16, pk);
+      }
+    }
+    float a0, a1, a2, a3;
+    f2_unpack(acc0, a0, a1);
+    f2_unpack(acc1, a2, a3);
+    l = l * alpha + ((a0 + a1) + (a2 + a3));
+    tc_wait_st();
+    tc_fence_before();
+    __syncthreads();  // P_j complete in TMEM (all 128 rows)
+    if (j == 0) ATTN_TRACE(3, attn_gtime());
+    if (issuer) {
+      tc_fence_after();
+      mbar_wait(v_full, ph);
+      const int nks = min(TKB / 16, (nvalid_blk + 15) / 16);  // 16-key steps holding valid keys
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t dv = make_sw128_desc(smem_u32(sV + ks * (16 * TD * 2)));
+        tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, ks > 0);
+      }
+      tc_commit(o_full);
+    }
+    mbar_wait(o_full, ph);
+    tc_fence_after();
+    if (j == 0) ATTN_TRACE(4, attn_gtime());
+    if (issuer && j + 1 < nkb) {  // the PV MMA has consumed V_j: prefetch V_{j+1}
+      mbar_arrive_expect_tx(v_full, kBlkBytes);
+      tma_load_2d(sV, &tm, v_full, 0, (2 * nh + h) * Tp + start + (j + 1) * TKB);
+    }
+    // O = alpha O + O_j  (the first block just takes O_0)
+    if (warp_active) {
+      const unsigned long long al2 = f2_pack(alpha, alpha);
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        tmem_ld_32x32b_x32(taddr + kOCol + hf * 32, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const unsigned long long oj = f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          o2[hf * 16 + i] = (j == 0) ? oj : f2_fma(o2[hf * 16 + i], al2, oj);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&q_empty[qs]);  // the slot's staging has been read
-      if (q == 0 && lane == 0) ATR(2, 25);
     }
-    if (q == 0 && lane == 0) ATR_DONE(2);
+    tc_fence_before();
+    __syncthreads();  // every row has read O_j before the next S MMA overwrites columns [0, 128)
+    if (j == 0) ATTN_TRACE(5, attn_gtime());
+  }
+  // epilogue: ctx = O / l (bf16).  Rows are staged in shared memory (sQ: the last S MMA has
+  // completed) with 16-byte chunks XOR-swizzled by row, then written back 4 rows per warp
+  // instruction, each row one contiguous 128-byte line (thread-per-row stores would touch 32
+  // lines per instruction).
+  {
+    float o[TD];
+#pragma unroll
+    for (int i = 0; i < TD / 2; ++i) f2_unpack(o2[i], o[2 * i], o[2 * i + 1]);
+    if constexpr (F8OUT) {  // 64-byte rows: 4 pieces, XOR-swizzled by row & 3
+      const float inv = ctx_scale / l;
+      uint4* srow = reinterpret_cast<uint4*>(sQ + row * TD);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        srow[k ^ (row & 3)] =
+            make_uint4(pack_e4m3x4(o[16 * k + 0] * inv, o[16 * k + 1] * inv, o[16 * k + 2] * inv, o[16 * k + 3] * inv),
+                       pack_e4m3x4(o[16 * k + 4] * inv, o[16 * k + 5] * inv, o[16 * k + 6] * inv, o[16 * k + 7] * inv),
+                       pack_e4m3x4(o[16 * k + 8] * inv, o[16 * k + 9] * inv, o[16 * k + 10] * inv, o[16 * k + 11] * inv),
+                       pack_e4m3x4(o[16 * k + 12] * inv, o[16 * k + 13] * inv, o[16 * k + 14] * inv,
+                                   o[16 * k + 15] * inv));
+    } else {
+      const float inv = 1.0f / l;
+      uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        srow[k ^ (row & 7)] = make_uint4(pack16x2<F16>(o[8 * k + 0] * inv, o[8 * k + 1] * inv),
+                                         pack16x2<F16>(o[8 * k + 2] * inv, o[8 * k + 3] * inv),
+                                         pack16x2<F16>(o[8 * k + 4] * inv, o[8 * k + 5] * inv),
+                                         pack16x2<F16>(o[8 * k + 6] * inv, o[8 * k + 7] * inv));
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(*tmem_slot);
+    tmem_dealloc<128>(tmem);
   }
+  {
+    const int nrows = min(TQ, L - q0);
+    if constexpr (F8OUT) {
+      uint8_t* c8 = reinterpret_cast<uint8_t*>(ctx);
+      const int c = lane & 3;
+      for (int rr = warp * 8 + (lane >> 2); rr < nrows; rr += 32) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * TD)[c ^ (rr & 3)];
+        *reinterpret_cast<uint4*>(c8 + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 16) = v;
+      }
+    } else {
+      const int c = lane & 7;
+      for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
+        *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+      }
+    }
+  }
+#ifdef ELIS_ATTN_TRACE
+  ATTN_TRACE(6, attn_gtime());
+  ATTN_TRACE(7, (static_cast<unsigned long long>(attn_smid()) << 32) | (static_cast<unsigned>(L) << 8) | nkb);
+#endif
 }
 
 // ============================================================================ CLS-only last layer
@@ -932,19 +657,20 @@ __global__ void __launch_bounds__(128) k_attention_cls(const uint16_t* __restric
 }  // namespace
 
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
-  // head-major planes [3 * nh][rows][64] viewed as one [3 * nh * rows, 64] matrix; 32-row boxes of
-  // 64 16-bit values (one SWIZZLE_128B row each): a request segment's rows of one head's Q, K or V
-  return make_tmap_bf16_box(m, qkv, rows * static_cast<uint64_t>(3 * (H / 64)), 64, 64, kBoxRows);
+  // 64 bf16 = 128 B inner box (one SWIZZLE_128B row), 128 rows
+  // head-major planes [3 * nh][rows][64] viewed as one [3 * nh * rows, 64] matrix: 128-token boxes of one
+  // head's Q, K or V are contiguous 16 KB blocks (64 bf16 = one SWIZZLE_128B row)
+  return make_tmap_bf16_box(m, qkv, rows * static_cast<uint64_t>(3 * (H / 64)), 64, 64, 128);
 }
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, int num_sms,
-                             cudaStream_t st) {
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
   const int64_t max_tiles = attn_max_tiles(T, n, attn_tile_q(d));
+  const unsigned grid = static_cast<unsigned>(max_tiles * num_heads);
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
     if (f16 && ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
@@ -954,14 +680,10 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
       if (e != cudaSuccess) return e;
     }
-    // persistent: one CTA per SM (TMEM 512 columns, shared memory ~194 KB), two pipelines each
-    const int64_t items = max_tiles * num_heads;
-    const unsigned grid = static_cast<unsigned>((items + 1) / 2 < num_sms ? (items + 1) / 2 : num_sms);
-    kern<<<grid, kAwsThreads, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
-                                                 static_cast<int>(plane_rows), ctx_f8_scale);
+    kern<<<grid, 128, kAttnTcSmem, st>>>(*tm_qkv, work, num_work, H, num_heads, ctx, scale_log2,
+                                         static_cast<int>(plane_rows), ctx_f8_scale);
   } else if (d == 32) {
     if (ctx_f8_scale > 0.f || f16) return cudaErrorInvalidValue;
-    const unsigned grid = static_cast<unsigned>(max_tiles * num_heads);
     k_attention<32><<<grid, 128, 0, st>>>(qkv, cu_seqlens, work, num_work, H, num_heads, ctx, scale_log2);
   } else {
     return cudaErrorInvalidValue;
@@ -986,5 +708,11 @@ cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens,
   return cudaGetLastError();
 }
 
+#ifdef ELIS_ATTN_TRACE
+extern "C" int elis_debug_attn_trace(unsigned long long* host, size_t n, int reset) {
+  if (reset) return static_cast<int>(cudaMemset(g_attn_trace_ptr(), 0, sizeof(g_attn_trace)));
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_attn_trace, std::min(n, kTraceCap * 8) * 8));
+}
+#endif
 
 }  // namespace elis

@@ -463,8 +463,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   if (!(cfg->residual_stream == ELIS_RESID_FP16)) ALLOC(p->h32, static_cast<size_t>(T) * H);  // residual16: the stream is hb
   ALLOC(p->hb, static_cast<size_t>(T) * H);
   ALLOC(p->qkv, static_cast<size_t>(T) * 3 * H);
-  // attention's 32-row TMA boxes read a few rows past a request's end; past the call's last token
-  // those rows must hold finite values (their P is 0, and 0 x NaN would not be)
+  // attention's 128-row TMA boxes read rows past a request's end; past the call's last token those
+  // rows must hold finite values (their P is 0, and 0 x NaN would not be)
   if (cudaMemset(p->qkv, 0, static_cast<size_t>(T) * 3 * H * sizeof(uint16_t)) != cudaSuccess)
     return cleanup_fail(ELIS_ERR_CUDA, "cudaMemset qkv");
   ALLOC(p->ctx, static_cast<size_t>(T) * H);
@@ -696,8 +696,7 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
     }
     LAUNCH(p, PC_ATTN, st,
            launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
-                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, p->num_sms,
-                            st));
+                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, st));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
@@ -1331,9 +1330,6 @@ static elis_status op_attention(const uint16_t* qkv, const int32_t* lengths, int
   if (d != 32 && d != 64) return fail(ELIS_ERR_INVALID_ARG, "head dim");
   if (f16 && d != 64) return fail(ELIS_ERR_INVALID_ARG, "fp16 attention needs head dim 64");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int dev = 0, num_sms = 148;
-  CUDA_TRY(cudaGetDevice(&dev));
-  CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   const int tq = attn_tile_q(d);
   const int64_t tiles = attn_work_capacity(T, n, tq);
   CUtensorMap tm{};
@@ -1348,7 +1344,7 @@ static elis_status op_attention(const uint16_t* qkv, const int32_t* lengths, int
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(AttnWork)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, f16, num_sms, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, f16, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);

@@ -75,27 +75,16 @@ bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, 
 cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st);
 
 // ---- varlen metadata / embedding / LayerNorm (norm.cu)
-// One attention tile (the request bounds travel with it: no dependent cu_seqlens load).
-//   long request (len[0] > 128, head dim 64) or any request at head dim 32: q rows
-//     [q0, q0 + tile_q) of the request at token `start[0]` with `len[0]` tokens, nreq = 1;
-//   packed short requests (head dim 64): nreq <= 4 requests of <= 128 tokens each, request k in
-//     32-row segments [f_k, f_k + ceil(len[k] / 32)) of one 128-row tile (f_0 = 0, f_{k+1} =
-//     f_k + ceil(len[k] / 32) <= 4), q0 = 0.  A request attends only to its own keys
-//     (block-diagonal mask) and its arithmetic does not depend on f_k (32-key aligned chunks).
+// One attention work item: q rows [q0, q0 + tile_q) of the request at token offset `start`
+// with `len` tokens (the request bounds travel with the item: no dependent cu_seqlens load).
 struct __align__(16) AttnWork {
-  int32_t start[4];
-  int16_t len[4];
-  int16_t q0, nreq;
-  int32_t req;  // index of the tile's first request
+  int32_t start, len, q0, req;
 };
-static_assert(sizeof(AttnWork) == 32, "AttnWork layout");
 // Work-list cost classes: keys a tile attends to, in 128-key blocks (1..4 for L <= 512).
 constexpr int kAttnCostClasses = 4;
 // lengths[n] -> cu_seqlens[n+1], attention work list with q tiles of tile_q rows in
 // descending cost class (longest-processing-time-first: the long tiles start in the first
 // wave, the short ones fill the tail), and its size; validates lengths and their sum.
-// tile_q == 128 (head dim 64): requests of <= 128 tokens are packed greedily, in index order
-// within each metadata thread's contiguous range, into tiles of <= 4 requests / 4 segments.
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
                         AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st);
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
@@ -110,25 +99,21 @@ cudaError_t launch_layernorm(const float* u, const float* gamma, const float* be
                              float* out32, uint16_t* outb, cudaStream_t st);
 
 // ---- attention (attention.cu)
-// head dim 64: persistent tcgen05 kernel with 128-row q tiles (short requests packed); head dim
-// 32: mma.sync, 64-row tiles.
+// head dim 64: tcgen05 kernel with 128-row q tiles; head dim 32: mma.sync, 64-row tiles.
 inline int attn_tile_q(int head_dim) { return head_dim == 64 ? 128 : 64; }
 // upper bound on the number of q-tiles for T tokens in n requests
 inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q - 1) / tile_q + n; }
 // total work-list entries to allocate for (T, n)
 inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_max_tiles(T, n, tile_q); }
-// head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 32-row boxes, SWIZZLE_128B
+// head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
-// head dim 64: persistent grid (2 CTAs per SM), CTA c takes items c, c + grid, ... of the
-// (work item, head) sequence, head fastest, so the list's cost order is the processing order;
-// head dim 32: one CTA per (work item, head)
+// grid: one CTA per (work item, head), head fastest, so the list's cost order is the launch order
 // head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H].
 // ctx_f8_scale > 0 (head dim 64 only): ctx is written as E4M3(ctx_f8_scale * ctx) bytes [T, H];
 // f16 (head dim 64 only): qkv and ctx are fp16 instead of bf16
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, int num_sms,
-                             cudaStream_t st);
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st);
 
 // CLS-only last layer: per (request, head) the attention of the CLS
 // query row (row cu[i]) over the request's keys, from the head-major qkv planes; writes the

@@ -56,30 +56,16 @@ __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict
   __syncthreads();
   // cost class: 128-key blocks a q tile of this request attends to
   auto cls = [](int L) { return min(kAttnCostClasses - 1, (L - 1) / 128); };
-  // 128-row tiles pack the requests of <= 128 tokens: greedy over this thread's range in index
-  // order; a pack closes when the next request's 32-row segments or a fifth request would not fit
-  const bool pack = tile_q == 128;
-  auto is_short = [&](int L) { return pack && L <= 128; };
-  // >= 16 consecutive requests per thread, so packs can form at any n
-  const int per = max(16, (n + kMetaThreads - 1) / kMetaThreads);
+  const int per = (n + kMetaThreads - 1) / kMetaThreads;
   const int i0 = min(n, static_cast<int>(threadIdx.x) * per), i1 = min(n, i0 + per);
   int my_len = 0, my_tiles[kAttnCostClasses] = {};
   uint32_t e = 0;
-  int psegs = 0, preq = 0;  // the open pack
   for (int i = i0; i < i1; ++i) {
     int L = lengths[i];
     if (L < 1 || L > max_position) { e |= ERR_LENGTH; L = max(1, min(L, max_position)); }
     my_len += L;
-    if (is_short(L)) {
-      const int sg = (L + 31) / 32;
-      if (preq == 4 || psegs + sg > 4) { ++my_tiles[0]; psegs = 0; preq = 0; }
-      psegs += sg;
-      ++preq;
-    } else {
-      my_tiles[cls(L)] += (L + tile_q - 1) / tile_q;
-    }
+    my_tiles[cls(L)] += (L + tile_q - 1) / tile_q;
   }
-  if (preq > 0) ++my_tiles[0];
   if (e) atomicOr(&s_err, e);
   const int len_off = block_exclusive_scan(my_len, warp_tot, &s_total_len);
   int tile_off[kAttnCostClasses];
@@ -94,46 +80,18 @@ __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict
     base += s_total_tiles[c];
   }
   int lo = len_off;
-  AttnWork pk{};  // the open pack
-  psegs = 0;
-  preq = 0;
-  auto flush = [&]() {
-    for (int k = pk.nreq; k < 4; ++k) { pk.start[k] = 0; pk.len[k] = 0; }
-    work[tile_off[0]++] = pk;
-    psegs = 0;
-    preq = 0;
-  };
   for (int i = i0; i < i1; ++i) {
     int L = max(1, min(lengths[i], max_position));
     cu[i] = lo;
     if (ok) {
-      if (is_short(L)) {
-        const int sg = (L + 31) / 32;
-        if (preq == 4 || psegs + sg > 4) flush();
-        if (preq == 0) { pk.q0 = 0; pk.req = i; }
-        pk.start[preq] = lo;
-        pk.len[preq] = static_cast<int16_t>(L);
-        pk.nreq = static_cast<int16_t>(++preq);
-        psegs += sg;
-      } else {
-        const int c = cls(L);
-        const int nt = (L + tile_q - 1) / tile_q;
-        AttnWork* dst = work + tile_off[c];
-        for (int t = 0; t < nt; ++t) {
-          AttnWork w{};
-          w.start[0] = lo;
-          w.len[0] = static_cast<int16_t>(L);
-          w.q0 = static_cast<int16_t>(t * tile_q);
-          w.nreq = 1;
-          w.req = i;
-          dst[t] = w;
-        }
-        tile_off[c] += nt;
-      }
+      const int c = cls(L);
+      const int nt = (L + tile_q - 1) / tile_q;
+      AttnWork* dst = work + tile_off[c];
+      for (int t = 0; t < nt; ++t) dst[t] = AttnWork{lo, L, t * tile_q, i};
+      tile_off[c] += nt;
     }
     lo += L;
   }
-  if (ok && preq > 0) flush();
   if (threadIdx.x == 0) {
     cu[n] = s_total_len;
     num_work[0] = ok ? base : 0;
