@@ -176,8 +176,13 @@ struct elis_predictor {
   std::vector<Layer> layers;
   std::vector<float*> head_w, head_b;
   std::vector<int> head_dims;
+  // 3xTF32 head (fc_tc_supported shapes): head_w[j] holds tf32(W), head_wl[j] = W - tf32(W); one
+  // tensor-core plan per hidden layer (head_tc empty: the exact-FFMA k_fc_f32 path)
+  std::vector<float*> head_wl;
+  std::vector<FcTcPlan> head_tc;
+  float *pooled_lo = nullptr, *z0_lo = nullptr, *z1_lo = nullptr;
 
-  // workspaces
+  // workspaces (pooled / z0 / z1: the hi halves when the head runs on the tensor cores)
   float *h32 = nullptr, *pooled = nullptr, *z0 = nullptr, *z1 = nullptr;
   float2* gx_stats = nullptr;  // FFN2 LN statistics through global memory (GemmArgs::gstats / gflag)
   uint32_t* gx_flag = nullptr;
@@ -458,6 +463,19 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
     in = o;
   }
   p->head_dims.push_back(1);
+  // hidden head layers on the tensor cores (3xTF32) when every one has a supported shape
+  bool head_tc = true;
+  for (int j = 0; j + 1 < cfg->head_layers; ++j) head_tc = head_tc && fc_tc_supported(cfg->head_hidden, p->head_dims[j]);
+  if (head_tc) {
+    for (int j = 0; j + 1 < cfg->head_layers; ++j) {
+      float* wl = nullptr;
+      const size_t cnt = static_cast<size_t>(cfg->head_hidden) * p->head_dims[j];
+      ALLOC(wl, cnt);
+      if (launch_split_tf32(p->head_w[j], wl, cnt, nullptr) != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "split head weights");
+      p->head_wl.push_back(wl);
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup_fail(ELIS_ERR_CUDA, "split head weights");
+  }
 
   // ---- workspaces
   if (!(cfg->residual_stream == ELIS_RESID_FP16)) ALLOC(p->h32, static_cast<size_t>(T) * H);  // residual16: the stream is hb
@@ -489,6 +507,24 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   ALLOC(p->pooled, static_cast<size_t>(N) * H);
   ALLOC(p->z0, static_cast<size_t>(N) * cfg->head_hidden);
   ALLOC(p->z1, static_cast<size_t>(N) * cfg->head_hidden);
+  if (!p->head_wl.empty()) {
+    ALLOC(p->pooled_lo, static_cast<size_t>(N) * H);
+    ALLOC(p->z0_lo, static_cast<size_t>(N) * cfg->head_hidden);
+    ALLOC(p->z1_lo, static_cast<size_t>(N) * cfg->head_hidden);
+    const float* xh = p->pooled;
+    const float* xl = p->pooled_lo;
+    float* yh[2] = {p->z0, p->z1};
+    float* yl[2] = {p->z0_lo, p->z1_lo};
+    for (int j = 0; j + 1 < cfg->head_layers; ++j) {
+      FcTcPlan f{};
+      if (!make_fc_tc_plan(&f, xh, xl, static_cast<uint64_t>(N), p->head_w[j], p->head_wl[j], p->head_b[j], yh[j & 1],
+                           yl[j & 1], cfg->head_hidden, p->head_dims[j]))
+        return cleanup_fail(ELIS_ERR_CUDA, "head tensor maps");
+      p->head_tc.push_back(f);
+      xh = yh[j & 1];
+      xl = yl[j & 1];
+    }
+  }
   ALLOC(p->fc_part, kFcPartCap);
   ALLOC(p->fc_ctr, kFcCtrCap);
   p->key_cap = std::max(N, 65536);
@@ -629,7 +665,8 @@ elis_status elis_predict_remaining_dist(elis_predictor* p, const int32_t* tokens
     pa.max_pairs = p->cfg.max_requests;
     pa.epoch = p->pred_epoch;
     pa.ticket = p->pred_ticket;
-    LAUNCH(p, PC_ALLGATHER, st, launch_head_out_dist(nullptr, nullptr, nullptr, 0, 0, table, nullptr, pa, p->err, st));
+    LAUNCH(p, PC_ALLGATHER, st,
+           launch_head_out_dist(nullptr, nullptr, nullptr, nullptr, 0, 0, table, nullptr, pa, p->err, st));
     return ELIS_OK;
   }
   // NCCL: pairs of this rank (slot -1 padded) -> ncclAllGather -> scatter into the table
@@ -701,20 +738,29 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
   }
+  const bool tc = !p->head_tc.empty();
   if (c.cls_last_layer)  // row i of the compact buffer is request i's CLS row
-    LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st));
+    LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo));
   else
     LAUNCH(p, PC_POOL, st,
-           c.residual_stream == ELIS_RESID_FP16 ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st)
-                        : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st));
+           c.residual_stream == ELIS_RESID_FP16
+               ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo)
+               : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo));
   const float* x = p->pooled;
+  const float* xl = p->pooled_lo;  // nullptr on the FFMA path
   float* bufs[2] = {p->z0, p->z1};
+  float* bufs_lo[2] = {p->z0_lo, p->z1_lo};
   const int nl = c.head_layers;
   for (int j = 0; j < nl - 1; ++j) {
     float* y = bufs[j & 1];
-    const FcWork wk{p->fc_part, kFcPartCap, p->fc_ctr, kFcCtrCap, p->num_sms};
-    LAUNCH(p, PC_HEAD_FC, st,
-           launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st));
+    if (tc) {
+      LAUNCH(p, PC_HEAD_FC, st, launch_fc_tf32(p->head_tc[j], n, 1, st));
+      xl = bufs_lo[j & 1];
+    } else {
+      const FcWork wk{p->fc_part, kFcPartCap, p->fc_ctr, kFcCtrCap, p->num_sms};
+      LAUNCH(p, PC_HEAD_FC, st,
+             launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st));
+    }
     x = y;
   }
   if (mode == HEAD_DIST_PEER) {
@@ -726,11 +772,11 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
     pa.epoch = p->pred_epoch;
     pa.ticket = p->pred_ticket;
     LAUNCH(p, PC_HEAD_OUT, st,
-           launch_head_out_dist(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
+           launch_head_out_dist(x, xl, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
                                 pa, p->err, st));
   } else {
     LAUNCH(p, PC_HEAD_OUT, st,
-           launch_head_out(x, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
+           launch_head_out(x, xl, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
                            mode == HEAD_DIST_NCCL ? p->pred_send : nullptr, st));
   }
   return ELIS_OK;
@@ -1377,6 +1423,30 @@ elis_status elis_op_layernorm(const float* u, const float* gamma, const float* b
 elis_status elis_op_fc_f32(const float* X, const float* W, const float* b, float* Y, int32_t n, int32_t N, int32_t K,
                            int32_t relu, void* stream) {
   if (!X || !W || !b || !Y || n < 0 || N < 1 || K < 1) return fail(ELIS_ERR_INVALID_ARG, "fc arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n > 0 && fc_tc_supported(N, K)) {
+    // the predictor's path for these shapes: 3xTF32 on the tensor cores (X, W split here; Y = Yh + Yl)
+    float *xh, *xl, *wh, *wl, *yh, *yl;
+    const size_t nx = static_cast<size_t>(n) * K, nw = static_cast<size_t>(N) * K, ny = static_cast<size_t>(n) * N;
+    CUDA_TRY(cudaMalloc(&xh, nx * 4));
+    CUDA_TRY(cudaMalloc(&xl, nx * 4));
+    CUDA_TRY(cudaMalloc(&wh, nw * 4));
+    CUDA_TRY(cudaMalloc(&wl, nw * 4));
+    CUDA_TRY(cudaMalloc(&yh, ny * 4));
+    CUDA_TRY(cudaMalloc(&yl, ny * 4));
+    CUDA_TRY(cudaMemcpyAsync(xh, X, nx * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(wh, W, nw * 4, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(launch_split_tf32(xh, xl, nx, st));
+    CUDA_TRY(launch_split_tf32(wh, wl, nw, st));
+    FcTcPlan f{};
+    if (!make_fc_tc_plan(&f, xh, xl, static_cast<uint64_t>(n), wh, wl, b, yh, yl, N, K))
+      return fail(ELIS_ERR_CUDA, "tensor map encode");
+    CUDA_TRY(launch_fc_tf32(f, n, relu, st));
+    CUDA_TRY(launch_add_f32(yh, yl, Y, ny, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (float* q : {xh, xl, wh, wl, yh, yl}) cudaFree(q);
+    return ELIS_OK;
+  }
   // test entry: one process-wide split-K workspace (op calls are serialised by the caller)
   static float* part = nullptr;
   static uint32_t* ctr = nullptr;
@@ -1389,7 +1459,7 @@ elis_status elis_op_fc_f32(const float* X, const float* W, const float* b, float
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const FcWork wk{part, kFcPartCap, ctr, kFcCtrCap, sms};
-  CUDA_TRY(launch_fc_f32(X, W, b, Y, n, N, K, relu, wk, static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(launch_fc_f32(X, W, b, Y, n, N, K, relu, wk, st));
   return ELIS_OK;
 }
 

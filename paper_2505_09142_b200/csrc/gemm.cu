@@ -818,6 +818,12 @@ bool make_tmap_bf16_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+bool make_tmap_f32_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                       uint32_t box_rows) {
+  return make_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ptr, rows, cols, box_cols, box_rows,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 bool make_gemm_plan(GemmPlan* g, const void* A, uint64_t a_rows, const void* W, const float* bias,
                     const float* resid, void* out, int M, int N, int K, int epi) {
   if (N % 128 != 0 || K % BK != 0 || M < 0) return false;

@@ -128,11 +128,12 @@ cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens,
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, const uint32_t* err,
                                 float* dst, cudaStream_t st);
+// pooled_lo != nullptr: pooled is written as the 3xTF32 pair (pooled = tf32(p), pooled_lo = p - pooled)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
-                        float* pooled, cudaStream_t st);
+                        float* pooled, cudaStream_t st, float* pooled_lo = nullptr);
 // mean / CLS pooling over the fp16 residual stream (elis_config.residual16)
 cudaError_t launch_pool16(const uint16_t* h16, const int32_t* cu_seqlens, int n, int H, int pooling,
-                          const uint32_t* err, float* pooled, cudaStream_t st);
+                          const uint32_t* err, float* pooled, cudaStream_t st, float* pooled_lo = nullptr);
 cudaError_t launch_f16_to_f32(const uint16_t* src, float* dst, int64_t count, cudaStream_t st);
 // split-K workspace of the exact-fp32 head (part == nullptr: no split)
 struct FcWork {
@@ -145,9 +146,30 @@ struct FcWork {
 int fc_splits(int n, int N, int K, int num_sms, size_t part_cap, int ctr_cap);
 cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,
                           const FcWork& wk, cudaStream_t st);
+// 3xTF32 tensor-core head layer (kind::tf32): Y = relu?(X W^T + b) with X = Xh + Xl, W = Wh + Wl
+// (hi = tf32 rounding, lo = the fp32 remainder) and Y written as the same kind of pair; 128 x 64
+// tiles, K in 4 chunks over a cluster of 4 CTAs reduced in chunk order (batch-invariant).
+struct FcTcPlan {
+  CUtensorMap ah, al, bh, bl;
+  const float* bias;
+  float *yh, *yl;
+  int N, K;
+};
+bool fc_tc_supported(int N, int K);
+bool make_fc_tc_plan(FcTcPlan* f, const float* Xh, const float* Xl, uint64_t x_rows, const float* Wh, const float* Wl,
+                     const float* bias, float* Yh, float* Yl, int N, int K);
+cudaError_t launch_fc_tf32(const FcTcPlan& f, int n, int relu, cudaStream_t st);
+// in place: x <- tf32(x), lo <- x - tf32(x)
+cudaError_t launch_split_tf32(float* x, float* lo, size_t count, cudaStream_t st);
+// y = a + b (the pair recombined, exact)
+cudaError_t launch_add_f32(const float* a, const float* b, float* y, size_t count, cudaStream_t st);
+// fp32 [rows, cols] row-major, box {box_cols (<= 32 for SWIZZLE_128B), box_rows}, SWIZZLE_128B
+bool make_tmap_f32_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                       uint32_t box_rows);
 // out_pairs (optional): (out_slot[i], y_i) also written to out_pairs[i] (the NCCL exchange's send buffer)
-cudaError_t launch_head_out(const float* Z, const float* w, const float* b, int n, int K, float* out_pred,
-                            const int32_t* out_slot, int2* out_pairs, cudaStream_t st);
+// Zl != nullptr: the input row is Z + Zl (the 3xTF32 layers' pair)
+cudaError_t launch_head_out(const float* Z, const float* Zl, const float* w, const float* b, int n, int K,
+                            float* out_pred, const int32_t* out_slot, int2* out_pairs, cudaStream_t st);
 // table[pairs[j].x] = pairs[j].y for every pair with x >= 0 (the NCCL exchange's receive side)
 cudaError_t launch_scatter_pairs(const int2* pairs, int count, float* table, cudaStream_t st);
 
@@ -236,8 +258,8 @@ struct PredPeerArgs {
 // region over NVLink; the last CTA to finish publishes this rank's count + epoch flag to every
 // rank (release, system scope), acquires every rank's flag (bounded; ERR_PEER_TIMEOUT) and
 // scatters the other ranks' pairs into the local table.  n may be 0 (the rank still exchanges).
-cudaError_t launch_head_out_dist(const float* Z, const float* w, const float* b, int n, int K, float* table,
-                                 const int32_t* slot, PredPeerArgs pa, uint32_t* err, cudaStream_t st);
+cudaError_t launch_head_out_dist(const float* Z, const float* Zl, const float* w, const float* b, int n, int K,
+                                 float* table, const int32_t* slot, PredPeerArgs pa, uint32_t* err, cudaStream_t st);
 cudaError_t launch_select_dist_peer(const unsigned long long* keys, const uint32_t* local_info, int n_local, int cap,
                                     int global_offset, PeerArgs pa, const uint8_t* running,
                                     unsigned long long* mkeys, int32_t* mids, int32_t* out_ids, int32_t* out_count,
