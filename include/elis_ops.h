@@ -26,6 +26,14 @@ typedef enum {
 elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias, const float* residual,
                          void* out, int32_t M, int32_t N, int32_t K, int32_t epilogue, void* stream);
 
+/* fp16 operand precision (elis_config.precision = ELIS_PREC_FP16, the library default at head dim 64):
+ * the same tcgen05 GEMM with fp16 A [M, K] / W [N, K] and fp16 output.  epilogue ELIS_EPI_BIAS_BF16
+ * (here: fp16 out = A W^T + bias; the QKV projection) or ELIS_EPI_BIAS_GELU_BF16 (fp16 GELU_erf; FFN1).
+ * head_major = 1 (bias epilogue): out is written as the attention's head-major planes
+ * [N / 64][M][64] (the predictor's QKV layout).  N % 256 == 0, K % 64 == 0. */
+elis_status elis_op_gemm_f16(const uint16_t* A, const uint16_t* W, const float* bias, void* out, int32_t M, int32_t N,
+                             int32_t K, int32_t epilogue, int32_t head_major, void* stream);
+
 /* tcgen05 GEMM with the fused residual + LayerNorm epilogue (attention-output / FFN2 of a
  * post-LN BERT block): v = A W^T + bias + resid_inout; resid_inout <- LN(v; gamma, beta, eps)
  * (fp32, in place) and outb <- bf16(LN(v)).  N / (N % 256 ? 128 : 256) <= 4 (one cluster per row). */

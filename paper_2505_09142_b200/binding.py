@@ -107,6 +107,7 @@ def lib():
         "elis_profile_enable": (_i32, [_vp, _i32]),
         "elis_profile_read": (_i32, [_vp, _vp, _vp, _vp, _i32]),
         "elis_op_gemm": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]),
+        "elis_op_gemm_f16": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
         "elis_op_gemm_ln": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _f32, _vp, _i32, _i32, _i32, _vp]),
         "elis_op_quant_rows_e4m3": (_i32, [_vp, _i32, _i32, _vp, _vp, _f32, _vp]),
         "elis_op_gemm_f8": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32, _vp]),
@@ -363,6 +364,13 @@ def op_gemm_ln_f8(A, W, colscale, bias, resid_inout, gamma, beta, eps: float, ou
     check(lib().elis_op_gemm_ln_f8(_ptr(A), _ptr(W), _ptr(colscale), _ptr(bias), _ptr(resid_inout), _ptr(gamma),
                                    _ptr(beta), eps, _ptr(outb), out_scale, M, N, K, _stream(stream)),
           "elis_op_gemm_ln_f8")
+
+
+def op_gemm_f16(A, W, bias, out, epilogue: int, head_major: bool = False, stream=None):
+    M, K = A.shape
+    N = W.shape[0]
+    check(lib().elis_op_gemm_f16(_ptr(A), _ptr(W), _ptr(bias), _ptr(out), M, N, K, epilogue, int(head_major),
+                                 _stream(stream)), "elis_op_gemm_f16")
 
 
 def op_attention(qkv, lengths, hidden: int, num_heads: int, ctx, stream=None, f16: bool = False):

@@ -22,6 +22,8 @@
 
 #include "../../include/elis.h"
 #include "../../include/elis_ops.h"
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -464,7 +466,8 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   }
   p->head_dims.push_back(1);
   // hidden head layers on the tensor cores (3xTF32) when every one has a supported shape
-  bool head_tc = true;
+  // (ELIS_HEAD_FFMA=1: diagnostics -- keep the exact-FFMA k_fc_f32 path)
+  bool head_tc = !(getenv("ELIS_HEAD_FFMA") && atoi(getenv("ELIS_HEAD_FFMA")) == 1);
   for (int j = 0; j + 1 < cfg->head_layers; ++j) head_tc = head_tc && fc_tc_supported(cfg->head_hidden, p->head_dims[j]);
   if (head_tc) {
     for (int j = 0; j + 1 < cfg->head_layers; ++j) {
@@ -825,10 +828,9 @@ elis_status elis_isrtf_select(elis_predictor* p, const float* pred, const int32_
          launch_make_keys(pred, generated, order, running, n, policy, allow, p->cfg.head_predicts_total, 0u,
                           starvation_of(pre), p->sc.keys, p->sc.info, st));
   LAUNCH(p, PC_SELECT, st,
-         launch_select_topk(p->sc.keys, nullptr, n, batch_cap, out_ids, pre ? pre->out_count : nullptr,
-                            pre ? pre->out_nan_count : nullptr, p->sc, st));
-  if (pre && pre->out_preempted)
-    LAUNCH(p, PC_PREEMPT, st, launch_preempt_flags(p->sc.keys, running, n, p->sc.info, pre->out_preempted, st));
+         launch_select_cluster(p->sc.keys, n, batch_cap, out_ids, pre ? pre->out_count : nullptr,
+                               pre ? pre->out_nan_count : nullptr, running, pre ? pre->out_preempted : nullptr, p->sc,
+                               st));
   return ELIS_OK;
 }
 
@@ -1269,6 +1271,24 @@ elis_status elis_op_gemm(const uint16_t* A, const uint16_t* W, const float* bias
   if (epilogue == ELIS_EPI_BIAS_RESID_F32 && !residual) return fail(ELIS_ERR_INVALID_ARG, "residual is NULL");
   GemmPlan g;
   if (!make_gemm_plan(&g, A, M, W, bias, residual, out, M, N, K, epilogue))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUDA_TRY(launch_gemm(g, sms, static_cast<cudaStream_t>(stream)));
+  return ELIS_OK;
+}
+
+elis_status elis_op_gemm_f16(const uint16_t* A, const uint16_t* W, const float* bias, void* out, int32_t M, int32_t N,
+                             int32_t K, int32_t epilogue, int32_t head_major, void* stream) {
+  if (!A || !W || !bias || !out || M < 1 || N < 256 || N % 256 || K < 64 || K % 64 || epilogue < 0 || epilogue > 1)
+    return fail(ELIS_ERR_INVALID_ARG, "gemm arguments");
+  if (head_major && (epilogue != ELIS_EPI_BIAS_BF16 || N % 64)) return fail(ELIS_ERR_INVALID_ARG, "head-major output");
+  GemmPlan g;
+  if (!make_gemm_plan(&g, A, M, W, bias, nullptr, out, M, N, K, epilogue))
+    return fail(ELIS_ERR_CUDA, "tensor map encode");
+  g.f16 = 1;
+  if (head_major && !gemm_plan_set_head_major(&g, out, static_cast<uint64_t>(M)))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

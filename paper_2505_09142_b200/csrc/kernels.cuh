@@ -197,6 +197,10 @@ cudaError_t launch_make_keys(const float* pred, const int32_t* generated, const 
 cudaError_t launch_select_topk(const unsigned long long* keys, const int32_t* ids, int n, int cap,
                                int32_t* out_ids, int32_t* out_count, int32_t* out_nan, SelectScratch sc,
                                cudaStream_t st);
+// single-node top-cap + preemption flags (out_preempted optional) over a cluster of <= 16 CTAs
+cudaError_t launch_select_cluster(const unsigned long long* keys, int n, int cap, int32_t* out_ids, int32_t* out_count,
+                                  int32_t* out_nan, const uint8_t* running, uint8_t* out_preempted, SelectScratch sc,
+                                  cudaStream_t st);
 cudaError_t launch_preempt_flags(const unsigned long long* keys, const uint8_t* running, int n, const uint32_t* info,
                                  uint8_t* out_preempted, cudaStream_t st);
 // per-node variants (node == nullptr: one node); out_ids [num_nodes * cap], out_count [num_nodes]

@@ -166,6 +166,7 @@ __device__ int cta_topk_sorted(const unsigned long long* keys, const int32_t* id
         }
         const int excl = incl - tot;
         const int need = s_remaining;
+        __syncwarp();  // every lane has read s_remaining before one of them rewrites it
         if (need > excl && need <= incl) {
           int run = excl;
 #pragma unroll
@@ -266,6 +267,236 @@ __global__ void __launch_bounds__(kSelThreads) k_select_topk(const unsigned long
     info_w[4] = static_cast<uint32_t>(target);
     info_w[5] = static_cast<uint32_t>(elig);
     if (out_nan && w == 0) *out_nan = static_cast<int32_t>(info[6]);
+  }
+}
+
+// ------------------------------------------------------------------------------ cluster select
+// The single-node select (elis_isrtf_select) over a cluster of C <= 16 CTAs (C = ceil(n / 4096)):
+// CTA r scans slots [r s, r s + s) (s = ceil(n / C); re-read from L1 every pass), and the
+// cluster agrees on every radix decision through DSMEM -- each CTA publishes its partial
+// (eligible count, min / max key; a 256-bin histogram per 8-bit digit pass) in its own shared
+// memory, one cluster barrier, then every CTA sums the C partials in rank order and takes the
+// same decision.  Winners (masked prefix <= the decided prefix) are written straight into CTA
+// 0's shared memory at their CTA's offset (rank-ordered prefix of the per-CTA counts), CTA 0
+// sorts them (bitonic) and writes the batch; every CTA writes the preemption flags of its own
+// slots (running && !selected) in the same launch.  Keys are unique, so the result is the exact
+// (deterministic) top-cap whatever the cluster size.
+constexpr int kSelClusterMax = 16, kSelClusterSlice = 4096;
+__global__ void __launch_bounds__(kSelThreads, 1)
+    k_select_cluster(const unsigned long long* __restrict__ keys, int n, int cap, int sort_len,
+                     int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count, int32_t* __restrict__ out_nan,
+                     const uint8_t* __restrict__ running, uint8_t* __restrict__ out_preempted,
+                     uint32_t* __restrict__ info, unsigned long long* __restrict__ sel_keys,
+                     int32_t* __restrict__ sel_ids) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  unsigned long long* ck = reinterpret_cast<unsigned long long*>(sm);  // [sort_len] (CTA 0)
+  int32_t* ci = reinterpret_cast<int32_t*>(ck + sort_len);             // [sort_len]
+  __shared__ int hist[2][256];
+  __shared__ int tot[256];
+  __shared__ unsigned long long s_min, s_max, g_prefix, g_mask;
+  __shared__ int s_elig, s_cnt, s_cursor, g_elig, g_remaining, g_digit, g_done, g_off, g_total;
+  const int tid = threadIdx.x, lane = lane_id();
+  const int C = static_cast<int>(gridDim.x);   // the whole grid is one cluster
+  const int r = static_cast<int>(cluster_ctarank());
+  const int slice = (n + C - 1) / C;
+  const int lo = min(n, r * slice), hi = min(n, lo + slice);
+  auto scan = [&](auto&& fn) {   // this CTA's slots, kSelBatch loads in flight per thread
+    for (int i0 = lo; i0 < hi; i0 += kSelBatch * kSelThreads) {
+      unsigned long long kb[kSelBatch];
+#pragma unroll
+      for (int u = 0; u < kSelBatch; ++u) {
+        const int i = i0 + u * kSelThreads + tid;
+        kb[u] = i < hi ? keys[i] : KEY_NONE;
+      }
+#pragma unroll
+      for (int u = 0; u < kSelBatch; ++u) {
+        const int i = i0 + u * kSelThreads + tid;
+        if (i < hi) fn(i, kb[u]);
+      }
+    }
+  };
+  // DSMEM address of this CTA's variable `v` in CTA q
+  auto peer = [](const void* v, int q) { return mapa_shared(smem_u32(v), static_cast<uint32_t>(q)); };
+  auto ld_u64 = [](uint32_t a) {
+    unsigned long long x;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(x) : "r"(a) : "memory");
+    return x;
+  };
+  auto ld_s32 = [](uint32_t a) {
+    int x;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(x) : "r"(a) : "memory");
+    return x;
+  };
+  if (tid == 0) { s_min = KEY_NONE; s_max = 0; s_elig = 0; s_cnt = 0; }
+  for (int b = tid; b < 256; b += kSelThreads) hist[0][b] = hist[1][b] = 0;
+  __syncthreads();
+  // ---- eligible count, min / max key over the cluster
+  {
+    int e = 0;
+    unsigned long long kmin = KEY_NONE, kmax = 0;
+    scan([&](int, unsigned long long k) {
+      if (k != KEY_NONE) { ++e; kmin = k < kmin ? k : kmin; kmax = k > kmax ? k : kmax; }
+    });
+    e = __reduce_add_sync(0xffffffffu, e);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+      kmin = a < kmin ? a : kmin;
+      kmax = b > kmax ? b : kmax;
+    }
+    if (lane == 0 && e) {
+      atomicAdd(&s_elig, e);
+      atomicMin(&s_min, kmin);
+      atomicMax(&s_max, kmax);
+    }
+  }
+  cluster_sync_all();
+  if (tid == 0) {
+    int e = 0;
+    unsigned long long mn = KEY_NONE, mx = 0;
+    for (int q = 0; q < C; ++q) {
+      e += ld_s32(peer(&s_elig, q));
+      const unsigned long long a = ld_u64(peer(&s_min, q)), b = ld_u64(peer(&s_max, q));
+      mn = a < mn ? a : mn;
+      mx = b > mx ? b : mx;
+    }
+    g_elig = e;
+    const int target = min(cap, e);
+    g_remaining = target;
+    g_done = 0;
+    g_prefix = 0;
+    g_mask = 0;
+    g_digit = 56;  // start shift
+    if (target > 0 && target < e) {  // >= 2 distinct (unique) keys: the radix starts at the first differing byte
+      const int top = 63 - __clzll(static_cast<long long>(mn ^ mx));
+      g_digit = (top >> 3) << 3;
+      if (g_digit < 56) {
+        g_mask = ~((1ull << (g_digit + 8)) - 1ull);
+        g_prefix = mn & g_mask;
+      }
+    }
+  }
+  __syncthreads();
+  const int elig = g_elig, target = min(cap, elig);
+  const bool take_all = target == elig;
+  // ---- MSB-first 8-bit radix select of the target-th key, decided identically by every CTA
+  if (target > 0 && !take_all) {
+    int pass = 0;
+    for (int shift = g_digit; shift >= 0; shift -= 8, ++pass) {
+      int* h = hist[pass & 1];
+      const unsigned long long prefix = g_prefix, mask = g_mask;
+      scan([&](int, unsigned long long k) {
+        if (k != KEY_NONE && (k & mask) == prefix) atomicAdd(&h[(k >> shift) & 255], 1);
+      });
+      cluster_sync_all();  // every CTA's histogram of this pass is complete (and the pass-2 buffer free)
+      for (int b = tid; b < 256; b += kSelThreads) {
+        int s = 0;
+        for (int q = 0; q < C; ++q) s += ld_s32(peer(&h[b], q));
+        tot[b] = s;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        int c[8], t = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c[q] = tot[8 * tid + q]; t += c[q]; }
+        int incl = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += y;
+        }
+        const int excl = incl - t, need = g_remaining;
+        __syncwarp();  // every lane has read the shared decision state before one of them rewrites it
+        if (need > excl && need <= incl) {
+          int run = excl;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (need > run && need <= run + c[q]) {
+              g_prefix = prefix | (static_cast<unsigned long long>(8 * tid + q) << shift);
+              g_mask = mask | (0xFFull << shift);
+              g_remaining = need - run;
+              g_done = (c[q] == need - run) ? 1 : 0;
+            }
+            run += c[q];
+          }
+        }
+      }
+      // the other buffer is reused next pass: zero it (its readers finished before this pass's barrier)
+      for (int b = tid; b < 256; b += kSelThreads) hist[(pass + 1) & 1][b] = 0;
+      __syncthreads();
+      if (g_done) break;
+    }
+  }
+  const unsigned long long prefix = g_prefix, mask = g_mask;
+  auto selected = [&](unsigned long long k) { return target > 0 && k != KEY_NONE && (take_all || (k & mask) <= prefix); };
+  // ---- winners: count, rank-ordered offsets, stores into CTA 0's arrays; preemption flags
+  int cnt = 0;
+  scan([&](int i, unsigned long long k) {
+    const bool s = selected(k);
+    cnt += s;
+    if (out_preempted) out_preempted[i] = (running && running[i] && !s) ? 1 : 0;
+  });
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0 && cnt) atomicAdd(&s_cnt, cnt);
+  cluster_sync_all();
+  if (tid == 0) {
+    int off = 0, all = 0;
+    for (int q = 0; q < C; ++q) {
+      const int c = ld_s32(peer(&s_cnt, q));
+      if (q < r) off += c;
+      all += c;
+    }
+    g_off = off;
+    g_total = all;
+    s_cursor = 0;  // (s_cnt stays intact: the peers read it after the same barrier)
+  }
+  __syncthreads();
+  const uint32_t ck0 = peer(ck, 0), ci0 = peer(ci, 0);
+  scan([&](int i, unsigned long long k) {
+    if (selected(k)) {
+      const int slot = g_off + atomicAdd(&s_cursor, 1);
+      if (slot < sort_len) {
+        asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ck0 + 8u * slot), "l"(k) : "memory");
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ci0 + 4u * slot), "r"(i) : "memory");
+      }
+    }
+  });
+  cluster_sync_all();  // CTA 0 holds every winner
+  if (r == 0) {
+    for (int i = g_total + tid; i < sort_len; i += kSelThreads) {
+      ck[i] = KEY_NONE;
+      ci[i] = -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= sort_len; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < sort_len / 2; i += kSelThreads) {
+          const int a = 2 * i - (i & (stride - 1)), b = a + stride;
+          const bool up = ((a & size) == 0);
+          const unsigned long long ka = ck[a], kb = ck[b];
+          if ((ka > kb) == up) {
+            ck[a] = kb; ck[b] = ka;
+            const int t = ci[a]; ci[a] = ci[b]; ci[b] = t;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int j = tid; j < cap; j += kSelThreads) {
+      const bool v = j < target;
+      out_ids[j] = v ? ci[j] : -1;
+      if (sel_keys) sel_keys[j] = v ? ck[j] : KEY_NONE;
+      if (sel_ids) sel_ids[j] = v ? ci[j] : -1;
+    }
+    if (tid == 0) {
+      if (out_count) *out_count = target;
+      const unsigned long long thr = target > 0 ? ck[target - 1] : 0ull;
+      info[0] = static_cast<uint32_t>(thr);
+      info[1] = static_cast<uint32_t>(thr >> 32);
+      info[4] = static_cast<uint32_t>(target);
+      info[5] = static_cast<uint32_t>(elig);
+      if (out_nan) *out_nan = static_cast<int32_t>(info[6]);
+    }
   }
 }
 
@@ -510,6 +741,37 @@ cudaError_t launch_select_topk_nodes(const unsigned long long* keys, const int32
   k_select_topk<<<num_nodes, kSelThreads, smem, st>>>(keys, ids, node, node_ready, n, cap, out_ids, out_count,
                                                       out_nan, sc.info, node ? nullptr : sc.sel_keys,
                                                       node ? nullptr : sc.sel_ids, sort_len);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_cluster(const unsigned long long* keys, int n, int cap, int32_t* out_ids, int32_t* out_count,
+                                  int32_t* out_nan, const uint8_t* running, uint8_t* out_preempted, SelectScratch sc,
+                                  cudaStream_t st) {
+  const int sort_len = next_pow2(cap < 2 ? 2 : cap);
+  const size_t smem = static_cast<size_t>(sort_len) * (sizeof(unsigned long long) + sizeof(int32_t));
+  if (!attr_once(reinterpret_cast<const void*>(k_select_cluster))) {  // per device
+    cudaError_t e = cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kMaxBatchCap * 12 + 1024));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  int C = (n + kSelClusterSlice - 1) / kSelClusterSlice;
+  C = C < 1 ? 1 : (C > kSelClusterMax ? kSelClusterMax : C);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kSelThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_select_cluster, keys, n, cap, sort_len, out_ids, out_count, out_nan,
+                                     running, out_preempted, sc.info, sc.sel_keys, sc.sel_ids);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

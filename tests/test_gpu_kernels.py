@@ -23,6 +23,12 @@ def bf16_tensor(x: np.ndarray):
     return torch.from_numpy(x).to(torch.bfloat16).cuda(), x.astype(np.float64)
 
 
+def fp16_tensor(x: np.ndarray):
+    """fp16-representable fp32 numpy -> (torch fp16 on cuda, exact fp64 numpy copy)."""
+    t = torch.from_numpy(np.asarray(x, np.float32)).to(torch.float16)
+    return t.cuda(), t.float().numpy().astype(np.float64)
+
+
 def to_np(t):
     return t.detach().float().cpu().numpy().astype(np.float64)
 
@@ -73,6 +79,29 @@ def test_gemm_tcgen05_parity(cuda_lib, M, N, K, epi):
         np.testing.assert_allclose(to_np(out), ref, rtol=1e-5, atol=1e-4)
 
 
+@pytest.mark.parametrize("M", [1, 129, 300, 1000, 4099])
+@pytest.mark.parametrize("N,K,epi,hm", [(2304, 768, 0, True), (2304, 768, 0, False), (3072, 768, 1, False),
+                                        (3072, 1024, 0, True), (4096, 1024, 1, False)])
+def test_gemm_f16_parity(cuda_lib, M, N, K, epi, hm):
+    """The fp16 instantiations the bench runs (QKV with the head-major store, FFN1 + GELU): fp32
+    accumulation then one fp16 rounding of the output (rel 2^-11 = 4.9e-4)."""
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    rng = np.random.default_rng(M * 3 + N + K + epi)
+    A, A64 = fp16_tensor(rng.normal(0, 1, (M, K)))
+    W, W64 = fp16_tensor(rng.normal(0, 0.05, (N, K)))
+    b64 = rng.normal(0, 0.1, N).astype(np.float32)
+    ref = oenc.linear(A64, W64, b64.astype(np.float64))
+    if epi == 1:
+        ref = oenc.gelu(ref)
+    out = torch.full((M * N,), float("nan"), dtype=torch.float16, device="cuda")
+    binding.op_gemm_f16(A, W, torch.from_numpy(b64).cuda(), out, epi, head_major=hm)
+    torch.cuda.synchronize()
+    got = to_np(out)
+    got = got.reshape(N // 64, M, 64).transpose(1, 0, 2).reshape(M, N) if hm else got.reshape(M, N)
+    np.testing.assert_allclose(got, ref, rtol=2e-3, atol=5e-4 if epi == 0 else 8e-4)
+
+
 @pytest.mark.parametrize("d,nh", [(64, 12), (32, 4), (64, 16)])
 def test_attention_varlen_parity(cuda_lib, d, nh):
     from paper_2505_09142_b200 import binding
@@ -93,12 +122,6 @@ def test_attention_varlen_parity(cuda_lib, d, nh):
         ref = oenc.attention(qkv64[sl, :H], qkv64[sl, H:2 * H], qkv64[sl, 2 * H:], nh)
         err = np.abs(got[sl] - ref).max()
         assert err < 2e-2, (i, int(L), err)
-
-
-def fp16_tensor(x: np.ndarray):
-    """fp16-representable fp32 numpy -> (torch fp16 on cuda, exact fp64 numpy copy)."""
-    t = torch.from_numpy(np.asarray(x, np.float32)).to(torch.float16)
-    return t.cuda(), t.float().numpy().astype(np.float64)
 
 
 # lengths that exercise the packed short-request tiles (several requests of <= 128 tokens per
