@@ -309,6 +309,36 @@ elis_status elis_iteration_table_host(elis_predictor* p, const int32_t* h_tokens
 elis_status elis_cost_split(const int32_t* lengths, int32_t n, int32_t world, int32_t num_layers, int32_t hidden,
                             int32_t intermediate, int32_t* out_bounds);
 
+/* ---- device-resident token arena of the in-flight table ---------
+ * PAPER.md Sec. 3.4 sends each prompt to the scheduler once and then only the fixed-window partial
+ * outputs; the predictor re-encodes "the prompt attached with the answer"
+ * whenever the job returns to the Job Pool (Alg. 1 lines 10-18).  The arena keeps, in
+ * device memory, every slot's prompt ([CLS] ... [SEP], 1..512 tokens) and its 512 most recent
+ * response tokens; per iteration the caller uploads only new prompts and the tokens each
+ * returning job generated, and gathers the due set's predictor inputs on the device:
+ *   prompt ++ response                      if |prompt| + generated <= max_len,
+ *   prompt[:max_len - k] ++ last k response otherwise, k = min(generated, 254)   (R7).
+ * All arrays are DEVICE pointers, work is enqueued on `stream`.  Device-detected errors (slot
+ * outside [0, max_slots), a prompt length outside [1, 512], a negative count, gathering a slot with
+ * no prompt) are sticky, reported by elis_arena_sync_status. */
+typedef struct elis_arena elis_arena;
+elis_status elis_arena_create(int32_t max_slots, int32_t device, elis_arena** out);
+void elis_arena_destroy(elis_arena* a);
+/* slots [m]: slot k gets prompt tokens[offset_k .. offset_k + lengths[k]) (packed back to back in
+ * slot order) and its generated count reset to 0. */
+elis_status elis_arena_set_prompts(elis_arena* a, const int32_t* slots, const int32_t* tokens,
+                                   const int32_t* lengths, int32_t m, void* stream);
+/* slots [m]: slot k appends counts[k] >= 0 generated tokens (packed back to back in slot order). */
+elis_status elis_arena_append(elis_arena* a, const int32_t* slots, const int32_t* tokens, const int32_t* counts,
+                              int32_t m, void* stream);
+/* Predictor inputs of the n due slots: out_lengths [n], out_tokens [sum] (packed, the layout
+ * elis_predict_remaining takes), out_dims [2] = {n, sum} (optional; e.g. for the total on the host
+ * or a graph).  out_tokens must hold n * max_len tokens.  max_len in [2, 512]. */
+elis_status elis_arena_gather(elis_arena* a, const int32_t* slots, int32_t n, int32_t max_len, int32_t* out_tokens,
+                              int32_t* out_lengths, int32_t* out_dims, void* stream);
+/* Synchronise `stream`, return (and clear) the arena's sticky error: ELIS_ERR_DEVICE_INPUT if set. */
+elis_status elis_arena_sync_status(elis_arena* a, void* stream);
+
 /* Synchronise the stream of the last call and return (and clear) the sticky device
  * error word: ELIS_ERR_DEVICE_INPUT if set, else ELIS_OK / ELIS_ERR_CUDA. */
 elis_status elis_sync_status(elis_predictor* p);

@@ -98,6 +98,12 @@ def lib():
         "elis_iteration_table_host": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
                                              _vp]),
         "elis_cost_split": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _vp]),
+        "elis_arena_create": (_i32, [_i32, _i32, _vp]),
+        "elis_arena_destroy": (None, [_vp]),
+        "elis_arena_set_prompts": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
+        "elis_arena_append": (_i32, [_vp, _vp, _vp, _vp, _i32, _vp]),
+        "elis_arena_gather": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+        "elis_arena_sync_status": (_i32, [_vp, _vp]),
         "elis_sync_status": (_i32, [_vp]),
         "elis_last_device_error_bits": (_u32, [_vp]),
         "elis_status_string": (ctypes.c_char_p, [_i32]),
@@ -305,6 +311,44 @@ def peer_attach_local(predictors: list["Predictor"]):
     """Wire predictors of ONE process as ranks 0..world-1 of the peer-memory transport."""
     arr = (_vp * len(predictors))(*[P.h for P in predictors])
     check(lib().elis_peer_attach_local(arr, len(predictors)), "elis_peer_attach_local")
+
+
+class Arena:
+    """Owner of one elis_arena: the device-resident prompts and recent response tokens of an
+    in-flight table (include/elis.h).  Device tensors in, argument marshalling only."""
+
+    def __init__(self, max_slots: int, device: int = 0):
+        h = _vp()
+        check(lib().elis_arena_create(int(max_slots), int(device), ctypes.byref(h)), "elis_arena_create")
+        self.h = h
+        self.max_slots = max_slots
+
+    def close(self):
+        if self.h:
+            lib().elis_arena_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_prompts(self, slots, tokens, lengths, stream=None):
+        check(lib().elis_arena_set_prompts(self.h, _ptr(slots), _ptr(tokens), _ptr(lengths), int(slots.numel()),
+                                           _stream(stream)), "elis_arena_set_prompts")
+
+    def append(self, slots, tokens, counts, stream=None):
+        check(lib().elis_arena_append(self.h, _ptr(slots), _ptr(tokens), _ptr(counts), int(slots.numel()),
+                                      _stream(stream)), "elis_arena_append")
+
+    def gather(self, slots, max_len: int, out_tokens, out_lengths, out_dims=None, stream=None):
+        check(lib().elis_arena_gather(self.h, _ptr(slots), int(slots.numel()), int(max_len), _ptr(out_tokens),
+                                      _ptr(out_lengths), _ptr(out_dims) if out_dims is not None else None,
+                                      _stream(stream)), "elis_arena_gather")
+
+    def sync_status(self, stream=None) -> int:
+        return lib().elis_arena_sync_status(self.h, _stream(stream))
 
 
 def cost_split(lengths: np.ndarray, world: int, cfg: inputs.EncoderConfig) -> np.ndarray:

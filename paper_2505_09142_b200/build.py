@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "elis")
 LIB = os.path.join(PKG, "libelis.so")
-SOURCES = ["elis.cu", "gemm.cu", "attention.cu", "norm.cu", "head.cu", "select.cu"]
+SOURCES = ["elis.cu", "gemm.cu", "attention.cu", "norm.cu", "head.cu", "select.cu", "arena.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 
 NVCC_FLAGS = [

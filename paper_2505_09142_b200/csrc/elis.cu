@@ -1195,6 +1195,115 @@ elis_status elis_cost_split(const int32_t* lengths, int32_t n, int32_t world, in
   return ELIS_OK;
 }
 
+// ---- token arena (include/elis.h)
+}  // extern "C"
+struct elis_arena {
+  int device = 0;
+  int max_slots = 0;
+  int32_t *prompt = nullptr, *ring = nullptr, *plen = nullptr, *glen = nullptr;
+  int32_t *offsets = nullptr, *cu = nullptr;
+  int offsets_cap = 0, cu_cap = 0;
+  uint32_t* err = nullptr;
+  void release() {
+    for (void* q : {static_cast<void*>(prompt), static_cast<void*>(ring), static_cast<void*>(plen),
+                    static_cast<void*>(glen), static_cast<void*>(offsets), static_cast<void*>(cu),
+                    static_cast<void*>(err)})
+      if (q) cudaFree(q);
+  }
+  cudaError_t scratch(int32_t** buf, int* cap, int need) {
+    if (*cap >= need) return cudaSuccess;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(buf, static_cast<size_t>(need) * sizeof(int32_t));
+    if (e == cudaSuccess) *cap = need;
+    return e;
+  }
+};
+extern "C" {
+
+elis_status elis_arena_create(int32_t max_slots, int32_t device, elis_arena** out) {
+  if (!out || max_slots < 1) return fail(ELIS_ERR_INVALID_ARG, "arena arguments");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  elis_arena* a = new elis_arena();
+  a->device = device;
+  a->max_slots = max_slots;
+  const size_t big = static_cast<size_t>(max_slots) * kArenaLen * sizeof(int32_t);
+  if (cudaMalloc(&a->prompt, big) != cudaSuccess || cudaMalloc(&a->ring, big) != cudaSuccess ||
+      cudaMalloc(&a->plen, max_slots * sizeof(int32_t)) != cudaSuccess ||
+      cudaMalloc(&a->glen, max_slots * sizeof(int32_t)) != cudaSuccess || cudaMalloc(&a->err, 4) != cudaSuccess ||
+      cudaMemset(a->plen, 0, max_slots * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(a->glen, 0, max_slots * sizeof(int32_t)) != cudaSuccess || cudaMemset(a->err, 0, 4) != cudaSuccess) {
+    a->release();
+    delete a;
+    return fail(ELIS_ERR_OOM, "arena allocation");
+  }
+  *out = a;
+  return ELIS_OK;
+}
+
+void elis_arena_destroy(elis_arena* a) {
+  if (!a) return;
+  cudaSetDevice(a->device);
+  cudaDeviceSynchronize();
+  a->release();
+  delete a;
+}
+
+elis_status elis_arena_set_prompts(elis_arena* a, const int32_t* slots, const int32_t* tokens, const int32_t* lengths,
+                                   int32_t m, void* stream) {
+  if (!a || m < 0 || (m > 0 && (!slots || !tokens || !lengths))) return fail(ELIS_ERR_INVALID_ARG, "arena arguments");
+  if (m == 0) return ELIS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(a->device));
+  CUDA_TRY(a->scratch(&a->offsets, &a->offsets_cap, m));
+  CUDA_TRY(launch_arena_offsets(lengths, m, a->offsets, st));
+  CUDA_TRY(launch_arena_set(slots, tokens, lengths, a->offsets, m, a->max_slots, a->prompt, a->plen, a->glen, a->err, st));
+  return ELIS_OK;
+}
+
+elis_status elis_arena_append(elis_arena* a, const int32_t* slots, const int32_t* tokens, const int32_t* counts,
+                              int32_t m, void* stream) {
+  if (!a || m < 0 || (m > 0 && (!slots || !tokens || !counts))) return fail(ELIS_ERR_INVALID_ARG, "arena arguments");
+  if (m == 0) return ELIS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(a->device));
+  CUDA_TRY(a->scratch(&a->offsets, &a->offsets_cap, m));
+  CUDA_TRY(launch_arena_offsets(counts, m, a->offsets, st));
+  CUDA_TRY(launch_arena_append(slots, tokens, counts, a->offsets, m, a->max_slots, a->ring, a->glen, a->err, st));
+  return ELIS_OK;
+}
+
+elis_status elis_arena_gather(elis_arena* a, const int32_t* slots, int32_t n, int32_t max_len, int32_t* out_tokens,
+                              int32_t* out_lengths, int32_t* out_dims, void* stream) {
+  if (!a || n < 0 || max_len < 2 || max_len > kArenaLen || (n > 0 && (!slots || !out_tokens || !out_lengths)))
+    return fail(ELIS_ERR_INVALID_ARG, "arena arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaSetDevice(a->device));
+  if (n == 0) {
+    if (out_dims) CUDA_TRY(cudaMemsetAsync(out_dims, 0, 2 * sizeof(int32_t), st));
+    return ELIS_OK;
+  }
+  CUDA_TRY(a->scratch(&a->cu, &a->cu_cap, n + 1));
+  CUDA_TRY(launch_arena_gather(slots, n, a->max_slots, max_len, a->prompt, a->ring, a->plen, a->glen, out_lengths,
+                               a->cu, out_dims, out_tokens, a->err, st));
+  return ELIS_OK;
+}
+
+elis_status elis_arena_sync_status(elis_arena* a, void* stream) {
+  if (!a) return fail(ELIS_ERR_INVALID_ARG, "arena is NULL");
+  CUDA_TRY(cudaSetDevice(a->device));
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  uint32_t bits = 0;
+  CUDA_TRY(cudaMemcpy(&bits, a->err, 4, cudaMemcpyDeviceToHost));
+  if (bits) {
+    CUDA_TRY(cudaMemset(a->err, 0, 4));
+    return fail(ELIS_ERR_DEVICE_INPUT, "arena: slot out of range, prompt length outside [1, 512] or gather of an unset slot");
+  }
+  return ELIS_OK;
+}
+
 elis_status elis_sync_status(elis_predictor* p) {
   if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
   CUDA_TRY(cudaSetDevice(p->device));

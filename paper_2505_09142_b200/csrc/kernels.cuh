@@ -13,7 +13,8 @@ enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BI
        EPI_BIAS_RESID16_LN = 4 };
 
 // Device error bits (sticky; see elis.h).
-enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u, ERR_GX_TIMEOUT = 16u };
+enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u, ERR_GX_TIMEOUT = 16u,
+                  ERR_ARENA = 32u };
 
 // ---- GEMM (gemm.cu)
 struct GemmArgs {
@@ -172,6 +173,23 @@ cudaError_t launch_head_out(const float* Z, const float* Zl, const float* w, con
                             float* out_pred, const int32_t* out_slot, int2* out_pairs, cudaStream_t st);
 // table[pairs[j].x] = pairs[j].y for every pair with x >= 0 (the NCCL exchange's receive side)
 cudaError_t launch_scatter_pairs(const int2* pairs, int count, float* table, cudaStream_t st);
+
+// ---- device-resident token arena of the in-flight table (arena.cu)
+// per slot: prompt [kArenaLen] int32, ring of the kArenaLen most recent response tokens, prompt length,
+// tokens generated so far; the predictor input keeps the prompt head and the kArenaKeepResp most
+// recent response tokens when longer than max_len (R7)
+constexpr int kArenaLen = 512, kArenaKeepResp = 254;
+cudaError_t launch_arena_offsets(const int32_t* counts, int m, int32_t* offsets, cudaStream_t st);
+cudaError_t launch_arena_set(const int32_t* slots, const int32_t* tokens, const int32_t* lengths,
+                             const int32_t* offsets, int m, int max_slots, int32_t* prompt, int32_t* plen,
+                             int32_t* glen, uint32_t* err, cudaStream_t st);
+cudaError_t launch_arena_append(const int32_t* slots, const int32_t* tokens, const int32_t* counts,
+                                const int32_t* offsets, int m, int max_slots, int32_t* ring, int32_t* glen,
+                                uint32_t* err, cudaStream_t st);
+// lengths [n], cu [n + 1], dims = {n, total} (optional), out_tokens [total]
+cudaError_t launch_arena_gather(const int32_t* slots, int n, int max_slots, int max_len, const int32_t* prompt,
+                                const int32_t* ring, const int32_t* plen, const int32_t* glen, int32_t* lengths,
+                                int32_t* cu, int32_t* dims, int32_t* out_tokens, uint32_t* err, cudaStream_t st);
 
 // ---- ISRTF select (select.cu)
 constexpr int kMaxBatchCap = 4096;

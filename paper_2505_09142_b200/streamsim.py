@@ -6,7 +6,10 @@ Priority Buffers and the least-loaded balancer) with the GPU h
 loop.  At every scheduling instant:
   * the due set -- new arrivals and the jobs that just ran a window (lines 10-18; jobs waiting
     in the Priority Buffer keep their cached priority, R8) -- is re-predicted by
-    elis_predict_remaining straight into a device-resident in-flight table (out_slot);
+    elis_predict_remaining straight into a device-resident in-flight table (out_slot); its
+    predictor inputs are gathered on the device from the token arena (elis_arena_*: each prompt is
+    uploaded once at arrival and each window's generated tokens appended, the B200 analogue of
+    "the prompt is sent once ... fixed-window partial outputs", P:314-315);
   * elis_isrtf_select_nodes picks the next batch of every free node from its own queue
     (line 19) with the running flags of the node's previous batch (preemption,
     P:345-348) and optional aging / preemption margin (row f3);
@@ -18,8 +21,9 @@ its true length is known to the simulator only.
 Priority sources: "gpu" (the BGE + 8-FC predictor; random-init weights carry no length
 signal, so this measures the mechanics and the per-iteration GPU overhead), "oracle" (true
 remaining tokens: the SRTF bound, written into the table), "noisy" (SPEC's NoisyIterative:
-true length + Laplace error with the MAE schedule, a stand-in for the trained predictor) and
-policy FCFS.
+true length + Laplace error with the MAE schedule, a stand-in for the trained predictor), "sjf"
+(the true total length, a static key: shortest-job-first by the profiled length; run
+without preemption) and policy FCFS.
 
 Every GPU decision is recorded so tests can replay the run through the fp64 oracle simulator
 and require identical schedules.
@@ -69,6 +73,14 @@ def build_sequence(prompt: np.ndarray, response: np.ndarray, generated: int, max
     return np.concatenate([head, resp[resp.size - keep_resp:]]).astype(np.int32)
 
 
+def seq_len(prompt_len: int, generated: int, max_len: int = 512) -> int:
+    """Length of build_sequence's output (R7)."""
+    if prompt_len + generated <= max_len:
+        return prompt_len + generated
+    keep = min(generated, 254)
+    return min(prompt_len, max_len - keep) + keep
+
+
 class StreamSim:
     """Algorithm 1 over `workers` backend nodes with per-node Priority Buffers:
     arrivals go to the least-loaded node (elis_assign_nodes), every free node forms its batch
@@ -79,7 +91,8 @@ class StreamSim:
     def __init__(self, predictor: binding.Predictor | None, policy: int = POLICY_ISRTF, cap: int = 4,
                  window: int = inputs.WINDOW_K, ttft_ms: float = 0.0, tpot_ms: float = 1.0,
                  allow_preempt: bool = True, priority: str = "gpu", seed: int = 0, workers: int = 1,
-                 boost_after: int = 1, boost_amount: float = 0.0, preempt_margin: float = 0.0):
+                 boost_after: int = 1, boost_amount: float = 0.0, preempt_margin: float = 0.0,
+                 arena: bool = True):
         if priority == "gpu" and predictor is None and policy == POLICY_ISRTF:
             raise ValueError("priority='gpu' needs a predictor")
         self.P = predictor
@@ -87,6 +100,7 @@ class StreamSim:
         self.ttft, self.tpot, self.allow = ttft_ms, tpot_ms, allow_preempt
         self.priority, self.seed, self.W = priority, seed, workers
         self.boost_after, self.boost_amount, self.margin = boost_after, boost_amount, preempt_margin
+        self.use_arena = arena
 
     def run(self, prompts, totals, arrivals_ms, select_predictor: binding.Predictor | None = None) -> StreamResult:
         import torch
@@ -123,6 +137,12 @@ class StreamSim:
         h_ids = torch.empty(W * cap, dtype=torch.int32).pin_memory()
         h_cnt = torch.empty(W, dtype=torch.int32).pin_memory()
         aging = self.boost_amount != 0.0
+        gpu_pred = self.priority == "gpu" and self.policy == POLICY_ISRTF
+        arena = binding.Arena(nj) if (gpu_pred and self.use_arena) else None
+        plen = np.array([len(q) for q in prompts], np.int64)
+        d_seq = torch.empty(max(nj, 1) * 512 if arena is not None else 1, dtype=torch.int32, device=dev)
+        d_seqlen = torch.empty(max(nj, 1), dtype=torch.int32, device=dev)
+        app_slots, app_toks, app_cnts = [], [], []   # this iteration's generated tokens (arena appends)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         recorded = {}
         nxt = 0                                     # next job to arrive
@@ -138,6 +158,10 @@ class StreamSim:
                 if free_at[w] is not None and free_at[w] <= t:
                     running[node_of == w] = 0
                     for j in batch_of[w]:
+                        if arena is not None and gen[j] + tokens_of[w] < totals[j]:
+                            app_slots.append(j)
+                            app_toks.append(responses[j][gen[j]:gen[j] + tokens_of[w]])
+                            app_cnts.append(tokens_of[w])
                         gen[j] += tokens_of[w]
                         if gen[j] >= totals[j]:
                             finish[j] = free_at[w]
@@ -153,6 +177,17 @@ class StreamSim:
             while nxt + n_new < nj and arrivals_ms[nxt + n_new] <= t:
                 n_new += 1
             ev0.record(st)
+            if n_new and arena is not None:   # each prompt crosses PCIe once
+                arena.set_prompts(torch.arange(nxt, nxt + n_new, dtype=torch.int32).to(dev, non_blocking=True),
+                                  torch.from_numpy(np.concatenate(prompts[nxt:nxt + n_new]).astype(np.int32)).to(
+                                      dev, non_blocking=True),
+                                  torch.from_numpy(plen[nxt:nxt + n_new].astype(np.int32)).to(dev, non_blocking=True),
+                                  stream=st)
+            if app_slots:                      # ... and each window's generated tokens once
+                arena.append(torch.from_numpy(np.array(app_slots, np.int32)).to(dev, non_blocking=True),
+                             torch.from_numpy(np.concatenate(app_toks).astype(np.int32)).to(dev, non_blocking=True),
+                             torch.from_numpy(np.array(app_cnts, np.int32)).to(dev, non_blocking=True), stream=st)
+                app_slots, app_toks, app_cnts = [], [], []
             if n_new:
                 P.assign_nodes(d_load, n_new, d_newnode, stream=st)
                 node_of[nxt:nxt + n_new] = d_newnode[:n_new].cpu().numpy()
@@ -172,15 +207,26 @@ class StreamSim:
                 ev1.record(st)
                 continue
             if due and self.policy == POLICY_ISRTF:
-                if self.priority == "gpu":
+                if self.priority == "gpu" and arena is not None:
+                    # predictor inputs gathered on the device; the host knows their total from the
+                    # prompt lengths and generated counts (the same R7 rule)
+                    slots = torch.from_numpy(np.array(due, np.int32)).to(dev, non_blocking=True)
+                    total = int(sum(seq_len(int(plen[j]), int(gen[j])) for j in due))
+                    arena.gather(slots, 512, d_seq, d_seqlen[:len(due)], stream=st)
+                    P.predict_remaining(d_seq, d_seqlen[:len(due)], total, d_table, out_slot=slots, stream=st)
+                elif self.priority == "gpu":
                     seqs = [build_sequence(prompts[j], responses[j], int(gen[j])) for j in due]
                     lens = np.array([q.size for q in seqs], np.int32)
                     toks = torch.from_numpy(np.concatenate(seqs)).to(dev, non_blocking=True)
                     slots = torch.from_numpy(np.array(due, np.int32)).to(dev, non_blocking=True)
                     P.predict_remaining(toks, torch.from_numpy(lens).to(dev, non_blocking=True), int(lens.sum()),
                                         d_table, out_slot=slots, stream=st)
-                else:  # "oracle": true remaining tokens (SRTF bound); "noisy": SPEC NoisyIterative
-                    if self.priority == "noisy":
+                else:  # "oracle": true remaining tokens (SRTF bound); "noisy": SPEC NoisyIterative;
+                    # "sjf": the job's true total length, fixed for its lifetime (SJF by the
+                    # profiled length; R16 reading of SV)
+                    if self.priority == "sjf":
+                        rem = totals[due].astype(np.float32)
+                    elif self.priority == "noisy":
                         rem = np.array([inputs.noisy_remaining(j, int(totals[j]), int(gen[j]), self.seed)
                                         for j in due], np.float32)
                     else:
@@ -226,5 +272,8 @@ class StreamSim:
                 batch_of[w], tokens_of[w], free_at[w] = batch, tok, t + dur
                 iters += 1
             host_ms += (time.perf_counter() - h0) * 1e3
+        if arena is not None:
+            assert arena.sync_status(st) == 0, binding.lib().elis_last_error()
+            arena.close()
         return StreamResult(first, finish, np.asarray(arrivals_ms, float), iters, gpu_ms / max(selects, 1),
                             host_ms / max(selects, 1), due_total / max(selects, 1), recorded)

@@ -5,7 +5,9 @@ policy/source) with mean JCT, mean queueing delay and the per-iteration GPU over
 the paper's 11.04 ms average scheduling overhead on A100).
 
 Workload: lam13 profile (average latency 8,610.2 ms); rate =
-m x (1000 / 8610.2) x 4 requests/s (P:481, P:492), m in {1, 3, 5}; cap 4 (P:551); K = 50;
+m x (1000 / 8610.2) x 4 requests/s, m in {1, 3, 5} (m = 1 is one worker's
+nominal capacity, cap / average latency: rho >= 1 since windows end early; sub-saturation runs
+use m < 1, e.g. --mults 0.7,0.9); cap 4 (P:551); K = 50;
 TTFT = 5% of the average latency; TPOT back-solved so TTFT + TPOT x mean output = the average
 latency.  Random-init weights: the GPU predictor carries no length signal, so its JCT shows
 the mechanics; "oracle" (true remaining) is the SRTF bound the paper's trained predictor
@@ -41,7 +43,7 @@ def main():
     ap.add_argument("--precision", default=None, choices=["bf16", "fp16", "fp8"],
                     help="encoder operands (default: fp16 + fp16 residual stream for head dim 64, as bench.py)")
     ap.add_argument("--aging", default="", help="boost_after,boost_amount (e.g. 4,50)")
-    ap.add_argument("--sources", default="fcfs,isrtf_gpu,isrtf_noisy,isrtf_oracle")
+    ap.add_argument("--sources", default="fcfs,isrtf_gpu,isrtf_noisy,isrtf_oracle,sjf")
     args = ap.parse_args()
     starv = {}
     if args.aging:
@@ -56,7 +58,8 @@ def main():
     lat = inputs.MODEL_AVG_LATENCY_MS["lam13"]
     ttft = 0.05 * lat
     tpot = 0.95 * lat / float(totals.mean())
-    table = {"fcfs": (1, "gpu"), "isrtf_gpu": (0, "gpu"), "isrtf_noisy": (0, "noisy"), "isrtf_oracle": (0, "oracle")}
+    table = {"fcfs": (1, "gpu"), "isrtf_gpu": (0, "gpu"), "isrtf_noisy": (0, "noisy"), "isrtf_oracle": (0, "oracle"),
+             "sjf": (0, "sjf")}
     for W in [int(x) for x in args.workers.split(",")]:
         for m in [float(x) for x in args.mults.split(",")]:
             rate = W * m * inputs.average_request_rate(lat, args.cap)
@@ -65,10 +68,11 @@ def main():
             for name in args.sources.split(","):
                 policy, source = table[name]
                 S = StreamSim(P, policy=policy, cap=args.cap, ttft_ms=ttft, tpot_ms=tpot, priority=source,
-                              workers=W, **starv)
+                              workers=W, allow_preempt=(source != "sjf"), **starv)
                 res[name] = S.run(prompts, totals, arr).summary()
             f = res["fcfs"]["mean_jct_ms"]
-            out = {"config": f"cfg4 stream: {args.n} Poisson requests, {W} workers, rate {m}x per worker "
+            rho = rate / (W * args.cap * 1000.0 / lat)
+            out = {"offered_load_rho": round(rho, 3), "config": f"cfg4 stream: {args.n} Poisson requests, {W} workers, rate {m}x per worker "
                              f"({rate:.4f} req/s total), lam13 profile, cap {args.cap}, K 50, predictor {args.config} "
                              f"on GPU ({prec} operands{', fp16 residual' if prec == 'fp16' else ''})"
                              + (f", aging {starv}" if starv else ""),

@@ -42,7 +42,7 @@ def replay(totals, arr, policy, cap, ttft, tpot, allow, priority, workers=1, **s
 
 
 @pytest.mark.parametrize("source,policy,allow", [("gpu", 0, True), ("oracle", 0, True), ("gpu", 0, False),
-                                                 ("none", 1, True)])
+                                                 ("none", 1, True), ("sjf", 0, False)])
 def test_stream_sim_matches_oracle_replay(tiny_predictor, source, policy, allow):
     from oracle import sim
     from paper_2505_09142_b200.streamsim import StreamSim
@@ -53,6 +53,8 @@ def test_stream_sim_matches_oracle_replay(tiny_predictor, source, policy, allow)
     assert np.isfinite(res.finish).all() and (res.finish >= res.first).all()
     if source == "gpu" and policy == 0:
         prio = lambda job, g: res.recorded[(job.id, g)]
+    elif source == "sjf":
+        prio = lambda job, g: float(np.float32(job.total))   # the profiled total length
     else:
         prio = sim.oracle_remaining
     first, finish = replay(totals, arr, policy, 4, ttft, tpot, allow, prio)
@@ -98,3 +100,15 @@ def test_fcfs_multi_worker_matches_oracle(tiny_predictor):
     first, finish = replay(totals, arr, 1, 2, ttft, tpot, True, sim.oracle_remaining, 5)
     np.testing.assert_array_equal(res.first, first)
     np.testing.assert_array_equal(res.finish, finish)
+
+
+def test_token_arena_path_equals_host_sequences(tiny_predictor):
+    """The device-resident token arena (prompts uploaded once, generated tokens appended per window,
+    due set gathered on the device) feeds the predictor exactly the sequences the host path builds:
+    every recorded priority is bitwise equal."""
+    from paper_2505_09142_b200.streamsim import StreamSim
+    prompts, totals, arr, ttft, tpot = make_stream(150, 3.0, seed=4)
+    runs = [StreamSim(tiny_predictor, cap=4, ttft_ms=ttft, tpot_ms=tpot, arena=a).run(prompts, totals, arr)
+            for a in (True, False)]
+    assert runs[0].recorded == runs[1].recorded
+    np.testing.assert_array_equal(runs[0].finish, runs[1].finish)
