@@ -285,6 +285,17 @@ elis_status elis_predict_remaining_dist(elis_predictor* p, const int32_t* tokens
                                         int32_t n, int64_t total_tokens, float* table, const int32_t* out_slot,
                                         void* stream);
 
+/* Shape-agnostic elis_predict_remaining (SURVEY.md Sec. 3.2 "one CUDA graph for a variable due
+ * set"): n and total_tokens are read on the device from dims = {n, total_tokens} (DEVICE int32[2],
+ * e.g. written by elis_arena_gather), so the call can be captured into a CUDA graph once and
+ * replayed for every iteration whatever the due set's shape.  Every kernel is launched for the
+ * predictor's capacity (max_requests, max_tokens) and exits beyond the device values; results are
+ * bit-identical to elis_predict_remaining on the same inputs.  n = 0 predicts nothing.  Device-
+ * detected: n outside [0, max_requests] or total_tokens > max_tokens (sticky, bit 64), and the
+ * usual length / token / sum checks.  Local head output only (no _dist). */
+elis_status elis_predict_remaining_dev(elis_predictor* p, const int32_t* tokens, const int32_t* lengths,
+                                       const int32_t* dims, float* out_pred, const int32_t* out_slot, void* stream);
+
 /* One scheduling iteration over an in-flight table from HOST buffers (the end-to-end call):
  * H2D copy of this rank's due tokens / lengths / table slots, elis_predict_remaining (or _dist
  * when a transport is attached) into `table` through the slots, elis_isrtf_select over the whole
@@ -344,7 +355,8 @@ elis_status elis_arena_sync_status(elis_arena* a, void* stream);
 elis_status elis_sync_status(elis_predictor* p);
 /* Raw device error bits of the last elis_sync_status (1: token id out of range,
  * 2: length outside [1, max_position], 4: sum(lengths) != total_tokens, 8: peer timeout,
- * 16: a global-memory LayerNorm statistics exchange timed out -- ELIS_GEMM_GX / elis_op_gemm_ln16). */
+ * 16: a global-memory LayerNorm statistics exchange timed out -- ELIS_GEMM_GX / elis_op_gemm_ln16,
+ * 64: a shape-agnostic call's device dims exceed the capacity -- elis_predict_remaining_dev). */
 uint32_t elis_last_device_error_bits(elis_predictor* p);
 const char* elis_status_string(elis_status s);
 const char* elis_last_error(void);                 /* thread-local detail of the last failure */

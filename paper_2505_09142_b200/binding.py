@@ -83,6 +83,7 @@ def lib():
         "elis_predictor_create": (_i32, [_vp, _vp, _sz, ctypes.POINTER(_vp)]),
         "elis_predictor_destroy": (None, [_vp]),
         "elis_predict_remaining": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
+        "elis_predict_remaining_dev": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
         "elis_isrtf_select": (_i32, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
         "elis_nccl_unique_id": (_i32, [_vp]),
         "elis_dist_attach": (_i32, [_vp, _i32, _i32, _vp]),
@@ -204,6 +205,12 @@ class Predictor:
         n = int(lengths.shape[0])
         check(lib().elis_predict_remaining(self.h, _ptr(tokens), _ptr(lengths), n, int(total_tokens), _ptr(out_pred),
                                            _ptr(out_slot), _stream(stream)), "elis_predict_remaining")
+
+    def predict_remaining_dev(self, tokens, lengths, dims, out_pred, out_slot=None, stream=None):
+        """Shape-agnostic predict: n and total_tokens from the device tensor dims = [n, total]
+        (graph-capturable; buffers sized for max_requests / max_tokens)."""
+        check(lib().elis_predict_remaining_dev(self.h, _ptr(tokens), _ptr(lengths), _ptr(dims), _ptr(out_pred),
+                                               _ptr(out_slot), _stream(stream)), "elis_predict_remaining_dev")
 
     def predict_remaining_dist(self, tokens, lengths, total_tokens: int, table, out_slot, stream=None):
         """This rank's due requests -> table[out_slot[i]] on EVERY attached rank (a collective)."""

@@ -577,9 +577,11 @@ __global__ void __launch_bounds__(128) k_attention_cls(const uint16_t* __restric
                                                        int nh, int Tp, int H, float scale_log2,
                                                        const float* __restrict__ h32, uint16_t* __restrict__ ctx_c,
                                                        float* __restrict__ hres_c, float ctx_scale,
-                                                       const uint32_t* __restrict__ err) {
+                                                       const uint32_t* __restrict__ err,
+                                                       const int32_t* __restrict__ dims) {
   if (err && *err) return;  // invalid lengths (sticky error): cu may point past the planes
   const int h = blockIdx.x, i = blockIdx.y;
+  if (i >= dev_n(dims, static_cast<int>(gridDim.y))) return;
   const int start = __ldg(cu + i), L = __ldg(cu + i + 1) - start;
   __shared__ float q[TD];
   __shared__ float p[512];
@@ -693,16 +695,16 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
 
 cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens, int n, int H, int num_heads,
                                  int64_t plane_rows, const float* h32, uint16_t* ctx_c, float* hres_c, int out_kind,
-                                 float ctx_scale, const uint32_t* err, cudaStream_t st) {
+                                 float ctx_scale, const uint32_t* err, cudaStream_t st, const int32_t* dims) {
   if (n <= 0) return cudaSuccess;
   if (H / num_heads != TD) return cudaErrorInvalidValue;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(TD));
   const dim3 grid(num_heads, n);
   const int Tp = static_cast<int>(plane_rows);
   switch (out_kind) {
-    case 0: k_attention_cls<0><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err); break;
-    case 1: k_attention_cls<1><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err); break;
-    case 2: k_attention_cls<2><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err); break;
+    case 0: k_attention_cls<0><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err, dims); break;
+    case 1: k_attention_cls<1><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err, dims); break;
+    case 2: k_attention_cls<2><<<grid, 128, 0, st>>>(qkv, cu_seqlens, num_heads, Tp, H, scale_log2, h32, ctx_c, hres_c, ctx_scale, err, dims); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -395,6 +395,16 @@ ELIS_DEV uint32_t pack_e4m3x4(float x0, float x1, float x2, float x3) {
 }
 
 
+// n / T of a shape-agnostic call (device dims = {n, total_tokens}; nullptr: keep the host values),
+// clamped to the capacity (the host values) the grid was sized for
+ELIS_DEV void dev_dims(const int32_t* dims, int& n, long long& T) {
+  if (dims) {
+    n = min(max(__ldg(dims), 0), n);
+    T = min(static_cast<long long>(max(__ldg(dims + 1), 0)), T);
+  }
+}
+ELIS_DEV int dev_n(const int32_t* dims, int n) { return dims ? min(max(__ldg(dims), 0), n) : n; }
+
 // Host: true if `fn`'s launch attributes were already set on the current device (then skip the
 // cudaFuncSetAttribute calls); records it otherwise.  Attributes are per device context.
 inline bool attr_once(const void* fn) {

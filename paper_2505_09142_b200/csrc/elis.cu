@@ -632,7 +632,7 @@ enum HeadOutMode { HEAD_LOCAL = 0, HEAD_DIST_PEER = 1, HEAD_DIST_NCCL = 2 };
 
 static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
                                 int64_t total_tokens, float* out_pred, const int32_t* out_slot, int mode,
-                                cudaStream_t st);
+                                cudaStream_t st, const int32_t* dims = nullptr);
 
 elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
                                    int64_t total_tokens, float* out_pred, const int32_t* out_slot, void* stream) {
@@ -645,6 +645,15 @@ elis_status elis_predict_remaining(elis_predictor* p, const int32_t* tokens, con
   CUDA_TRY(cudaSetDevice(p->device));
   return predict_impl(p, tokens, lengths, n, total_tokens, out_pred, out_slot, HEAD_LOCAL,
                       static_cast<cudaStream_t>(stream));
+}
+
+elis_status elis_predict_remaining_dev(elis_predictor* p, const int32_t* tokens, const int32_t* lengths,
+                                       const int32_t* dims, float* out_pred, const int32_t* out_slot, void* stream) {
+  if (!p) return fail(ELIS_ERR_INVALID_ARG, "predictor is NULL");
+  if (!tokens || !lengths || !dims || !out_pred) return fail(ELIS_ERR_INVALID_ARG, "NULL device array");
+  CUDA_TRY(cudaSetDevice(p->device));
+  return predict_impl(p, tokens, lengths, p->cfg.max_requests, p->cfg.max_tokens, out_pred, out_slot, HEAD_LOCAL,
+                      static_cast<cudaStream_t>(stream), dims);
 }
 
 elis_status elis_predict_remaining_dist(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
@@ -699,27 +708,32 @@ elis_status elis_predict_remaining_dist(elis_predictor* p, const int32_t* tokens
   return ELIS_OK;
 }
 
+// dims != nullptr (elis_predict_remaining_dev): n and total_tokens are the capacity the grids are sized
+// for, the actual values are read on the device from dims = {n, total}
 static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const int32_t* lengths, int32_t n,
                                 int64_t total_tokens, float* out_pred, const int32_t* out_slot, int mode,
-                                cudaStream_t st) {
+                                cudaStream_t st, const int32_t* dims) {
   const elis_config& c = p->cfg;
   const int H = c.hidden;
   const int M = static_cast<int>(total_tokens);
   const int64_t T_cap = c.max_tokens;  // rows of each head-major qkv plane
   p->last_stream = st;
-  p->last_T = total_tokens;
+  p->last_T = dims ? -1 : total_tokens;  // unknown on the host in a shape-agnostic call
   p->last_n = n;
+  const int32_t* M_dev = dims ? dims + 1 : nullptr;
 
   LAUNCH(p, PC_META, st,
-         launch_meta(lengths, n, total_tokens, c.max_position, p->cu, p->work, p->num_work, p->err, p->tile_q, st));
+         launch_meta(lengths, n, total_tokens, c.max_position, p->cu, p->work, p->num_work, p->err, p->tile_q, st,
+                     dims));
   LAUNCH(p, PC_EMBED, st,
          launch_embed_ln(tokens, p->cu, n, total_tokens, H, c.vocab_size, c.max_position, p->word, p->pos, p->type0,
                          p->emb_g, p->emb_b, c.ln_eps, p->h32, p->hb, p->err,
-                         c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, c.precision == ELIS_PREC_FP16, st));
+                         c.precision == ELIS_PREC_FP8 ? kF8ScaleHidden : 0.f, c.precision == ELIS_PREC_FP16, st, dims));
   const float f8_ctx = c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f;
   for (int l = 0; l < c.num_layers; ++l) {
     Layer& L = p->layers[l];
     L.p_qkv.args.M = L.p_out.args.M = L.p_ffn1.args.M = L.p_ffn2.args.M = M;
+    L.p_qkv.args.M_dev = L.p_out.args.M_dev = L.p_ffn1.args.M_dev = L.p_ffn2.args.M_dev = M_dev;
     LAUNCH(p, PC_QKV, st, launch_gemm(L.p_qkv, p->num_sms, st));
     if (c.cls_last_layer && l == c.num_layers - 1) {
       // CLS pooling: only row 0 of each request reaches the head, so the last layer's
@@ -727,8 +741,9 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
       const int kind = c.precision == ELIS_PREC_FP8 ? 2 : c.precision == ELIS_PREC_FP16 ? 1 : 0;
       LAUNCH(p, PC_ATTN, st,
              launch_attention_cls(p->qkv, p->cu, n, H, c.num_heads, T_cap, p->h32, p->ctx_c, p->hres_c, kind, f8_ctx,
-                                  p->err, st));
+                                  p->err, st, dims));
       p->c_out.args.M = p->c_ffn1.args.M = p->c_ffn2.args.M = n;
+      p->c_out.args.M_dev = p->c_ffn1.args.M_dev = p->c_ffn2.args.M_dev = dims;
       LAUNCH(p, PC_OUT, st, launch_gemm(p->c_out, p->num_sms, st));
       LAUNCH(p, PC_FFN1, st, launch_gemm(p->c_ffn1, p->num_sms, st));
       LAUNCH(p, PC_FFN2, st, launch_gemm(p->c_ffn2, p->num_sms, st));
@@ -743,12 +758,13 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
   }
   const bool tc = !p->head_tc.empty();
   if (c.cls_last_layer)  // row i of the compact buffer is request i's CLS row
-    LAUNCH(p, PC_POOL, st, launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo));
+    LAUNCH(p, PC_POOL, st,
+           launch_pool(p->hres_c, p->iota, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo, dims));
   else
     LAUNCH(p, PC_POOL, st,
            c.residual_stream == ELIS_RESID_FP16
-               ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo)
-               : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo));
+               ? launch_pool16(p->hb, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo, dims)
+               : launch_pool(p->h32, p->cu, n, H, c.pooling, p->err, p->pooled, st, p->pooled_lo, dims));
   const float* x = p->pooled;
   const float* xl = p->pooled_lo;  // nullptr on the FFMA path
   float* bufs[2] = {p->z0, p->z1};
@@ -757,12 +773,12 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
   for (int j = 0; j < nl - 1; ++j) {
     float* y = bufs[j & 1];
     if (tc) {
-      LAUNCH(p, PC_HEAD_FC, st, launch_fc_tf32(p->head_tc[j], n, 1, st));
+      LAUNCH(p, PC_HEAD_FC, st, launch_fc_tf32(p->head_tc[j], n, 1, st, dims));
       xl = bufs_lo[j & 1];
     } else {
       const FcWork wk{p->fc_part, kFcPartCap, p->fc_ctr, kFcCtrCap, p->num_sms};
       LAUNCH(p, PC_HEAD_FC, st,
-             launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st));
+             launch_fc_f32(x, p->head_w[j], p->head_b[j], y, n, c.head_hidden, p->head_dims[j], 1, wk, st, dims));
     }
     x = y;
   }
@@ -780,7 +796,7 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
   } else {
     LAUNCH(p, PC_HEAD_OUT, st,
            launch_head_out(x, xl, p->head_w[nl - 1], p->head_b[nl - 1], n, p->head_dims[nl - 1], out_pred, out_slot,
-                           mode == HEAD_DIST_NCCL ? p->pred_send : nullptr, st));
+                           mode == HEAD_DIST_NCCL ? p->pred_send : nullptr, st, dims));
   }
   return ELIS_OK;
 }

@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int M = args.M, N = args.N, K = args.K;
+  const int M = args.M_dev ? min(max(__ldg(args.M_dev), 0), args.M) : args.M;
+  const int N = args.N, K = args.K;
   const int num_m = (M + 2 * BM - 1) / (2 * BM);  // 256-row pair tiles
   const int num_n = N / BN;
   const int num_k = K / BKE;

@@ -14,7 +14,11 @@ enum { EPI_BIAS_BF16 = 0, EPI_BIAS_GELU_BF16 = 1, EPI_BIAS_RESID_F32 = 2, EPI_BI
 
 // Device error bits (sticky; see elis.h).
 enum : uint32_t { ERR_TOKEN = 1u, ERR_LENGTH = 2u, ERR_TOTAL = 4u, ERR_PEER_TIMEOUT = 8u, ERR_GX_TIMEOUT = 16u,
-                  ERR_ARENA = 32u };
+                  ERR_ARENA = 32u, ERR_DIMS = 64u };
+// device-side shape of a shape-agnostic call: dims = {n, total_tokens}, clamped to the capacity
+struct DevDims {
+  const int32_t* dims;  // nullptr: the host values
+};
 
 // ---- GEMM (gemm.cu)
 struct GemmArgs {
@@ -43,6 +47,9 @@ struct GemmArgs {
   int m_reverse;
   // sticky device error word (GX exchange timeout -> ERR_GX_TIMEOUT); nullptr: not reported
   uint32_t* err;
+  // shape-agnostic launches (elis_predict_remaining_dev): the row count is read from this device
+  // int (clamped to M, which is then the capacity the grid was sized for); nullptr: M
+  const int32_t* M_dev;
 };
 struct GemmPlan {
   CUtensorMap tmA;   // A operand, bf16 K-major
@@ -86,12 +93,17 @@ constexpr int kAttnCostClasses = 4;
 // lengths[n] -> cu_seqlens[n+1], attention work list with q tiles of tile_q rows in
 // descending cost class (longest-processing-time-first: the long tiles start in the first
 // wave, the short ones fill the tail), and its size; validates lengths and their sum.
+// dims (device {n, total}, optional): a shape-agnostic call -- n / total are read there and the host
+// values are the capacity (every launcher below that takes `dims` sizes its grid by the capacity and
+// exits beyond the device values)
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st);
+                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st,
+                        const int32_t* dims = nullptr);
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H,
                             int vocab, int max_position, const uint16_t* word, const uint16_t* pos,
                             const uint16_t* type0, const float* gamma, const float* beta, float eps, float* h32,
-                            uint16_t* hb, uint32_t* err, float f8_scale, bool f16, cudaStream_t st);
+                            uint16_t* hb, uint32_t* err, float f8_scale, bool f16, cudaStream_t st,
+                            const int32_t* dims = nullptr);
 // f8_scale > 0: hb receives E4M3(f8_scale * LN(x)) bytes [T, H] instead of bf16; f16: fp16
 // FP8 weights: q [rows, cols] = E4M3(W * 448 / amax_row), scale[row] = amax_row / 448 * post
 cudaError_t launch_quant_rows_e4m3(const float* W, int rows, int cols, uint8_t* q, float* scale, float post,
@@ -124,17 +136,18 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
 // then point past the token buffers)
 cudaError_t launch_attention_cls(const uint16_t* qkv, const int32_t* cu_seqlens, int n, int H, int num_heads,
                                  int64_t plane_rows, const float* h32, uint16_t* ctx_c, float* hres_c, int out_kind,
-                                 float ctx_scale, const uint32_t* err, cudaStream_t st);
+                                 float ctx_scale, const uint32_t* err, cudaStream_t st, const int32_t* dims = nullptr);
 
 // ---- pooling + regression head (head.cu)
 cudaError_t launch_scatter_rows(const float* src, const int32_t* cu_seqlens, int n, int H, const uint32_t* err,
                                 float* dst, cudaStream_t st);
 // pooled_lo != nullptr: pooled is written as the 3xTF32 pair (pooled = tf32(p), pooled_lo = p - pooled)
 cudaError_t launch_pool(const float* h32, const int32_t* cu_seqlens, int n, int H, int pooling, const uint32_t* err,
-                        float* pooled, cudaStream_t st, float* pooled_lo = nullptr);
+                        float* pooled, cudaStream_t st, float* pooled_lo = nullptr, const int32_t* dims = nullptr);
 // mean / CLS pooling over the fp16 residual stream (elis_config.residual16)
 cudaError_t launch_pool16(const uint16_t* h16, const int32_t* cu_seqlens, int n, int H, int pooling,
-                          const uint32_t* err, float* pooled, cudaStream_t st, float* pooled_lo = nullptr);
+                          const uint32_t* err, float* pooled, cudaStream_t st, float* pooled_lo = nullptr,
+                          const int32_t* dims = nullptr);
 cudaError_t launch_f16_to_f32(const uint16_t* src, float* dst, int64_t count, cudaStream_t st);
 // split-K workspace of the exact-fp32 head (part == nullptr: no split)
 struct FcWork {
@@ -146,7 +159,7 @@ struct FcWork {
 };
 int fc_splits(int n, int N, int K, int num_sms, size_t part_cap, int ctr_cap);
 cudaError_t launch_fc_f32(const float* X, const float* W, const float* b, float* Y, int n, int N, int K, int relu,
-                          const FcWork& wk, cudaStream_t st);
+                          const FcWork& wk, cudaStream_t st, const int32_t* dims = nullptr);
 // 3xTF32 tensor-core head layer (kind::tf32): Y = relu?(X W^T + b) with X = Xh + Xl, W = Wh + Wl
 // (hi = tf32 rounding, lo = the fp32 remainder) and Y written as the same kind of pair; 128 x 64
 // tiles, K in 4 chunks over a cluster of 4 CTAs reduced in chunk order (batch-invariant).
@@ -159,7 +172,7 @@ struct FcTcPlan {
 bool fc_tc_supported(int N, int K);
 bool make_fc_tc_plan(FcTcPlan* f, const float* Xh, const float* Xl, uint64_t x_rows, const float* Wh, const float* Wl,
                      const float* bias, float* Yh, float* Yl, int N, int K);
-cudaError_t launch_fc_tf32(const FcTcPlan& f, int n, int relu, cudaStream_t st);
+cudaError_t launch_fc_tf32(const FcTcPlan& f, int n, int relu, cudaStream_t st, const int32_t* dims = nullptr);
 // in place: x <- tf32(x), lo <- x - tf32(x)
 cudaError_t launch_split_tf32(float* x, float* lo, size_t count, cudaStream_t st);
 // y = a + b (the pair recombined, exact)
@@ -170,7 +183,8 @@ bool make_tmap_f32_box(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t 
 // out_pairs (optional): (out_slot[i], y_i) also written to out_pairs[i] (the NCCL exchange's send buffer)
 // Zl != nullptr: the input row is Z + Zl (the 3xTF32 layers' pair)
 cudaError_t launch_head_out(const float* Z, const float* Zl, const float* w, const float* b, int n, int K,
-                            float* out_pred, const int32_t* out_slot, int2* out_pairs, cudaStream_t st);
+                            float* out_pred, const int32_t* out_slot, int2* out_pairs, cudaStream_t st,
+                            const int32_t* dims = nullptr);
 // table[pairs[j].x] = pairs[j].y for every pair with x >= 0 (the NCCL exchange's receive side)
 cudaError_t launch_scatter_pairs(const int2* pairs, int count, float* table, cudaStream_t st);
 

@@ -48,11 +48,20 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total_out) {
 __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict__ lengths, int n, long long total,
                                                        int max_position, int32_t* __restrict__ cu,
                                                        AttnWork* __restrict__ work, int32_t* __restrict__ num_work,
-                                                       uint32_t* __restrict__ err, int tile_q) {
+                                                       uint32_t* __restrict__ err, int tile_q,
+                                                       const int32_t* __restrict__ dims) {
   __shared__ int warp_tot[32];
   __shared__ int s_total_len, s_total_tiles[kAttnCostClasses];
   __shared__ uint32_t s_err;
   if (threadIdx.x == 0) s_err = 0;
+  if (dims) {  // shape-agnostic call: n and total from the device, the host values are the capacity
+    const int dn = __ldg(dims), dt = __ldg(dims + 1);
+    if (dn < 0 || dn > n || dt > total) {
+      if (threadIdx.x == 0) s_err = ERR_DIMS;
+    }
+    n = min(max(dn, 0), n);
+    total = dt;
+  }
   __syncthreads();
   // cost class: 128-key blocks a q tile of this request attends to
   auto cls = [](int L) { return min(kAttnCostClasses - 1, (L - 1) / 128); };
@@ -98,6 +107,7 @@ __global__ void __launch_bounds__(kMetaThreads) k_meta(const int32_t* __restrict
     if (s_err) atomicOr(err, s_err);
   }
 }
+
 
 // ----------------------------------------------------------------------------- row helpers
 template <int H>
@@ -183,11 +193,12 @@ __global__ void __launch_bounds__(256) k_embed_ln(const int32_t* __restrict__ to
                                                   const uint16_t* __restrict__ type0, const float* __restrict__ gamma,
                                                   const float* __restrict__ beta, float eps, float* __restrict__ h32,
                                                   uint16_t* __restrict__ hb, uint32_t* __restrict__ err, float f8_scale,
-                                                  bool f16) {
+                                                  bool f16, const int32_t* __restrict__ dims) {
   using RL = RowLayout<H>;
   const int lane = lane_id();
   const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp_id();
-  if (t >= T) return;
+  dev_dims(dims, n, T);
+  if (t >= T || n < 1) return;
   // request containing token t: largest i with cu[i] <= t.  32-way search by the whole warp
   // (each lane probes one offset, a ballot picks the segment): 2 dependent loads for n <= 1024
   // instead of log2(n) for a binary search.  Invariant: cu[lo] <= t, answer in [lo, lo + len).
@@ -285,8 +296,9 @@ cudaError_t launch_quant_rows_e4m3(const float* W, int rows, int cols, uint8_t* 
 }
 
 cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_position, int32_t* cu_seqlens,
-                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st) {
-  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err, tile_q);
+                        AttnWork* work, int32_t* num_work, uint32_t* err, int tile_q, cudaStream_t st,
+                        const int32_t* dims) {
+  k_meta<<<1, kMetaThreads, 0, st>>>(lengths, n, total, max_position, cu_seqlens, work, num_work, err, tile_q, dims);
   return cudaGetLastError();
 }
 
@@ -301,11 +313,12 @@ cudaError_t launch_meta(const int32_t* lengths, int n, int64_t total, int max_po
 cudaError_t launch_embed_ln(const int32_t* tokens, const int32_t* cu_seqlens, int n, int64_t T, int H, int vocab,
                             int max_position, const uint16_t* word, const uint16_t* pos, const uint16_t* type0,
                             const float* gamma, const float* beta, float eps, float* h32, uint16_t* hb, uint32_t* err,
-                            float f8_scale, bool f16, cudaStream_t st) {
+                            float f8_scale, bool f16, cudaStream_t st, const int32_t* dims) {
   if (T <= 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
   ELIS_H_DISPATCH(H, (k_embed_ln<HH><<<grid, 256, 0, st>>>(tokens, cu_seqlens, n, T, vocab, max_position, word, pos,
-                                                            type0, gamma, beta, eps, h32, hb, err, f8_scale, f16)));
+                                                            type0, gamma, beta, eps, h32, hb, err, f8_scale, f16,
+                                                            dims)));
   return cudaGetLastError();
 }
 

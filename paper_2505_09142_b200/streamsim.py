@@ -92,7 +92,7 @@ class StreamSim:
                  window: int = inputs.WINDOW_K, ttft_ms: float = 0.0, tpot_ms: float = 1.0,
                  allow_preempt: bool = True, priority: str = "gpu", seed: int = 0, workers: int = 1,
                  boost_after: int = 1, boost_amount: float = 0.0, preempt_margin: float = 0.0,
-                 arena: bool = True):
+                 arena: bool = True, graph: bool = True):
         if priority == "gpu" and predictor is None and policy == POLICY_ISRTF:
             raise ValueError("priority='gpu' needs a predictor")
         self.P = predictor
@@ -101,6 +101,7 @@ class StreamSim:
         self.priority, self.seed, self.W = priority, seed, workers
         self.boost_after, self.boost_amount, self.margin = boost_after, boost_amount, preempt_margin
         self.use_arena = arena
+        self.use_graph = graph and arena
 
     def run(self, prompts, totals, arrivals_ms, select_predictor: binding.Predictor | None = None) -> StreamResult:
         import torch
@@ -122,7 +123,14 @@ class StreamSim:
         batch_of: list[list[int]] = [[] for _ in range(W)]
         tokens_of = [0] * W
         dev = torch.device("cuda")
-        st = torch.cuda.current_stream()
+        st = torch.cuda.Stream()             # a side stream: CUDA graphs cannot be captured on the default one
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            return self._loop(P, torch, dev, st, nj, W, cap, prompts, totals, arrivals_ms, responses, gen, node_of,
+                              waited, first, finish, running, started, free_at, batch_of, tokens_of)
+
+    def _loop(self, P, torch, dev, st, nj, W, cap, prompts, totals, arrivals_ms, responses, gen, node_of, waited,
+              first, finish, running, started, free_at, batch_of, tokens_of):
         d_table = torch.zeros(nj, device=dev)
         d_gen = torch.empty(nj, dtype=torch.int32, device=dev)
         d_run = torch.empty(nj, dtype=torch.uint8, device=dev)
@@ -143,6 +151,21 @@ class StreamSim:
         d_seq = torch.empty(max(nj, 1) * 512 if arena is not None else 1, dtype=torch.int32, device=dev)
         d_seqlen = torch.empty(max(nj, 1), dtype=torch.int32, device=dev)
         app_slots, app_toks, app_cnts = [], [], []   # this iteration's generated tokens (arena appends)
+        d_slots = torch.zeros(max(nj, 1), dtype=torch.int32, device=dev)
+        d_dims = torch.zeros(2, dtype=torch.int32, device=dev)
+        graph, eager_done = None, False
+
+        def predict_select():
+            # shape-agnostic predict (n, T from d_dims, written by the arena gather) + the select:
+            # one CUDA graph replayed every iteration whatever the due set's size
+            P.predict_remaining_dev(d_seq, d_seqlen, d_dims, d_table, out_slot=d_slots, stream=st)
+            select()
+
+        def select():
+            P.isrtf_select_nodes(d_table, d_gen, d_node, W, cap, d_ids, d_cnt, node_ready=d_ready,
+                                 policy=self.policy, allow_preempt=self.allow, order=d_order, running=d_run,
+                                 stream=st, windows_waited=d_wait if aging else None, boost_after=self.boost_after,
+                                 boost_amount=self.boost_amount, preempt_margin=self.margin)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         recorded = {}
         nxt = 0                                     # next job to arrive
@@ -207,7 +230,12 @@ class StreamSim:
                 ev1.record(st)
                 continue
             if due and self.policy == POLICY_ISRTF:
-                if self.priority == "gpu" and arena is not None:
+                if self.priority == "gpu" and arena is not None and self.use_graph:
+                    # predictor inputs gathered on the device (d_dims = {n, total}); predict + select
+                    # below, from the captured graph
+                    d_slots[:len(due)].copy_(torch.from_numpy(np.array(due, np.int32)), non_blocking=True)
+                    arena.gather(d_slots[:len(due)], 512, d_seq, d_seqlen, out_dims=d_dims, stream=st)
+                elif self.priority == "gpu" and arena is not None:
                     # predictor inputs gathered on the device; the host knows their total from the
                     # prompt lengths and generated counts (the same R7 rule)
                     slots = torch.from_numpy(np.array(due, np.int32)).to(dev, non_blocking=True)
@@ -238,10 +266,20 @@ class StreamSim:
             d_ready.copy_(torch.from_numpy(ready), non_blocking=True)
             if aging:
                 d_wait.copy_(torch.from_numpy(waited), non_blocking=True)
-            P.isrtf_select_nodes(d_table, d_gen, d_node, W, cap, d_ids, d_cnt, node_ready=d_ready,
-                                 policy=self.policy, allow_preempt=self.allow, order=d_order, running=d_run,
-                                 stream=st, windows_waited=d_wait if aging else None, boost_after=self.boost_after,
-                                 boost_amount=self.boost_amount, preempt_margin=self.margin)
+            if self.use_graph and gpu_pred:
+                if not due:
+                    d_dims.zero_()             # nothing to re-predict: the graph's predict is a no-op
+                if graph is None and eager_done:
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph, stream=st):
+                        predict_select()
+                if graph is not None:
+                    graph.replay()
+                else:                          # first iteration: eager (sets the launch attributes)
+                    predict_select()
+                    eager_done = True
+            else:
+                select()
             h_ids.copy_(d_ids, non_blocking=True)
             h_cnt.copy_(d_cnt, non_blocking=True)
             ev1.record(st)
