@@ -12,6 +12,7 @@
 // The whole K/V of one (request, head) is <= 512 x 64 x 2 x 2 B = 128 KB.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -269,6 +270,12 @@ ELIS_DEV unsigned long long f2_add(unsigned long long a, unsigned long long b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+ELIS_DEV unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+constexpr float kLazyRescale = 8.f;  // log2 units: P <= 2^8 before O is rescaled
 ELIS_DEV float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -563,6 +570,285 @@ __global__ void __launch_bounds__(128, 4)
 #endif
 }
 
+// ---------------------------------------------------------------------- 64-key-block engine (default)
+// Same CTA shape (128 q rows x one head, 4 warps, 4 CTAs per SM, 128 TMEM columns), keys in
+// blocks of 64 so that O can stay in TMEM:
+//   S_j = Q K_j^T        M 128 x N 64 x K 64 into TMEM columns [0, 64)
+//   softmax block j      one pass: the row's 64 scores read into registers (2 loads, one wait),
+//                        block max, lazy running max (it moves only when the block's exceeds it
+//                        by more than 2^8; then O is rescaled in TMEM), exp2, row sum, P packed
+//                        to 16 bits into columns [0, 32) over the consumed scores
+//   O += P_j V_j         A = P_j from TMEM, B = V_j (MN-major) from shared memory, accumulated in
+//                        TMEM columns [64, 128) across blocks; S_{j+1} is issued right behind it
+//                        (MMAs execute in issue order), so the next softmax waits for S only
+//   ctx = O / l          after the last block
+// No O in registers (the round-1 block of 128 keys folded O_j into 64 registers per thread, with
+// two serial TMEM passes per block).  K_{j+1} / V_{j+1} are loaded into the buffers of block
+// j - 1 as soon as S_j has completed (which implies PV_{j-1} did).  Measured (A/B, one session,
+// profiles/r02_ab_attention_64key.txt): cfg2 attention 1.58 / 1.53 vs 1.60 / 1.54 ms per step,
+// cfg5 8.42 vs 8.58 ms; ELIS_ATTN_ENGINE=128 selects the 128-key engine above.
+constexpr int TKB64 = 64;
+constexpr int kBlk64 = TKB64 * TD * 2;                        // 8 KB
+constexpr int kAttn64Smem = kBlkBytes + 4 * kBlk64 + 1024 + 256;  // Q, K[2], V[2]
+template <bool F8OUT, bool F16>
+__global__ void __launch_bounds__(128, 4)
+    k_attention_tc64(const __grid_constant__ CUtensorMap tm, const AttnWork* __restrict__ work,
+                     const int32_t* __restrict__ num_work, int H, int nh, uint16_t* __restrict__ ctx,
+                     float scale_log2, int Tp, float ctx_scale) {
+  const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
+  const AttnWork w = work[item];
+  if (item >= __ldg(num_work)) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* sQ = smem;                      // 128 rows
+  uint8_t* sK = sQ + kBlkBytes;            // [2][64 rows]
+  uint8_t* sV = sK + 2 * kBlk64;           // [2][64 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kBlk64);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;            // [2]
+  uint64_t* s_full = bars + 3;
+  uint64_t* o_full = bars + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+
+  const int start = w.start, L = w.len, q0 = w.q0;
+  const int nkb = (L + TKB64 - 1) / TKB64;  // 1..8
+  const int warp = warp_id(), lane = lane_id();
+  const bool issuer = threadIdx.x == 0;
+  const int rq = h * Tp + start, rk = (nh + h) * Tp + start, rv = (2 * nh + h) * Tp + start;
+  auto load_kv = [&](int j) {  // block j into buffer j & 1 (64-row boxes)
+    const int b = j & 1;
+    mbar_arrive_expect_tx(&kv_full[b], 2 * kBlk64);
+    tma_load_2d(sK + b * kBlk64, &tm, &kv_full[b], 0, rk + j * TKB64);
+    tma_load_2d(sV + b * kBlk64, &tm, &kv_full[b], 0, rv + j * TKB64);
+  };
+  if (issuer) {
+    tma_prefetch_desc(&tm);
+    mbar_init(q_full, 1);
+    mbar_init(&kv_full[0], 1);
+    mbar_init(&kv_full[1], 1);
+    mbar_init(s_full, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(q_full, kBlkBytes);
+    tma_load_2d(sQ, &tm, q_full, 0, rq + q0);
+    tma_load_2d(sQ + kBlk64, &tm, q_full, 0, rq + q0 + 64);
+    load_kv(0);
+    if (nkb > 1) load_kv(1);
+  }
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int row = warp * 32 + lane;
+  const bool warp_active = q0 + warp * 32 < L;
+  constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB64) : make_idesc_bf16_f32(TQ, TKB64);
+  constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);
+  const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+  if (issuer) {  // S_0
+    mbar_wait(q_full, 0);
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    const uint64_t dk = make_sw128_desc(smem_u32(sK));
+#pragma unroll
+    for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+    tc_commit(s_full);
+  }
+  float m = 0.f, l = 0.f;
+  const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
+  for (int j = 0; j < nkb; ++j) {
+    mbar_wait(s_full, j & 1);
+    tc_fence_after();
+    // S_j complete => PV_{j-1} complete: the buffers of block j - 1 take block j + 1
+    if (issuer && j >= 1 && j + 1 < nkb) load_kv(j + 1);
+    const int nk = min(TKB64, L - j * TKB64);   // valid keys of this block (keys >= L: other requests)
+    const int nch = (nk + 31) >> 5;             // 1..2
+    if (warp_active) {
+      uint32_t r[2][32];
+      tmem_ld_32x32b_x32(taddr, r[0]);
+      if (nch > 1) tmem_ld_32x32b_x32(taddr + 32, r[1]);
+      tc_wait_ld();
+      // the chunk holding the last valid key (if partial) is masked; each test names its chunk at
+      // compile time (no dynamic indexing of the score registers)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c < nch && nk < 32 * (c + 1)) {
+          const int tail = nk - 32 * c;
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e >= tail) r[c][e] = __float_as_uint(-INFINITY);
+        }
+      }
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(r[0][i]);
+#pragma unroll
+      for (int e = 8; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[0][e]), __uint_as_float(r[0][e + 1]));
+      if (nch > 1) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[1][e]), __uint_as_float(r[1][e + 1]));
+      }
+      const float bm = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+      const float ms = bm * scale_log2;  // finite: the block holds >= 1 valid key
+      float alpha = 1.f;
+      bool resc = false;
+      if (j == 0) {
+        m = ms;
+      } else if (ms > m + kLazyRescale) {  // rare: O rescaled below, once the scores are consumed
+        alpha = ex2_approx(m - ms);
+        m = ms;
+        l *= alpha;
+        resc = true;
+      }
+      const unsigned long long nm2 = f2_pack(-m, -m);
+      unsigned long long acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c < nch) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float x0, x1, p0, p1;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1])), sc2, nm2), x0, x1);
+            if (exp2_on_fma(e)) {
+              f2_unpack(exp2_poly2(x0, x1), p0, p1);
+            } else {
+              p0 = ex2_approx(x0);
+              p1 = ex2_approx(x1);
+            }
+            r[c][2 * e] = __float_as_uint(p0);
+            r[c][2 * e + 1] = __float_as_uint(p1);
+          }
+          if (nk < 32 * (c + 1)) {  // masked keys contribute exactly 0
+            const int tail = nk - 32 * c;
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e >= tail) r[c][e] = 0u;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            acc0 = f2_add(acc0, f2_pack(__uint_as_float(r[c][4 * e]), __uint_as_float(r[c][4 * e + 1])));
+            acc1 = f2_add(acc1, f2_pack(__uint_as_float(r[c][4 * e + 2]), __uint_as_float(r[c][4 * e + 3])));
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = pack16x2<F16>(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]));
+          tmem_st_32x32b_x16(taddr + c * 16, pk);
+        }
+      }
+      float a0, a1, a2, a3;
+      f2_unpack(acc0, a0, a1);
+      f2_unpack(acc1, a2, a3);
+      l += (a0 + a1) + (a2 + a3);
+      if (resc) {  // O (complete: PV_{j-1} preceded S_j) *= alpha, before PV_j is issued
+        const unsigned long long al2 = f2_pack(alpha, alpha);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(taddr + kOCol + x * 32, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float o0, o1;
+            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])), al2), o0, o1);
+            o[2 * i] = __float_as_uint(o0);
+            o[2 * i + 1] = __float_as_uint(o1);
+          }
+          tmem_st_32x32b_x32(taddr + kOCol + x * 32, o);
+        }
+      }
+      tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();  // P_j complete in TMEM (all 128 rows)
+    if (issuer) {
+      tc_fence_after();
+      const int b = j & 1;
+      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      const int nks = (nk + 15) / 16;  // 16-key steps holding valid keys
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t dv = make_sw128_desc(smem_u32(sV + b * kBlk64 + ks * (16 * TD * 2)));
+        tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, (j | ks) != 0 ? 1u : 0u);
+      }
+      if (j + 1 < nkb) {  // S_{j+1} right behind PV_j (in issue order: P_j is read before S overwrites it)
+        const int b1 = (j + 1) & 1;
+        mbar_wait(&kv_full[b1], ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        const uint64_t dk = make_sw128_desc(smem_u32(sK + b1 * kBlk64));
+#pragma unroll
+        for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+        tc_commit(s_full);
+      } else {
+        tc_commit(o_full);
+      }
+    }
+  }
+  mbar_wait(o_full, 0);
+  tc_fence_after();
+  // epilogue: ctx = O / l, staged in sQ (every MMA has completed), 4 rows per warp instruction
+  if (warp_active) {
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr + kOCol + x * 32, v);
+      tc_wait_ld();
+      if constexpr (F8OUT) {  // 64-byte rows: 4 pieces, XOR-swizzled by row & 3
+        const float inv = ctx_scale / l;
+        uint4* srow = reinterpret_cast<uint4*>(sQ + row * TD);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t* u = v + 16 * k;
+          srow[(2 * x + k) ^ (row & 3)] = make_uint4(
+              pack_e4m3x4(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv, __uint_as_float(u[2]) * inv,
+                          __uint_as_float(u[3]) * inv),
+              pack_e4m3x4(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv, __uint_as_float(u[6]) * inv,
+                          __uint_as_float(u[7]) * inv),
+              pack_e4m3x4(__uint_as_float(u[8]) * inv, __uint_as_float(u[9]) * inv, __uint_as_float(u[10]) * inv,
+                          __uint_as_float(u[11]) * inv),
+              pack_e4m3x4(__uint_as_float(u[12]) * inv, __uint_as_float(u[13]) * inv, __uint_as_float(u[14]) * inv,
+                          __uint_as_float(u[15]) * inv));
+        }
+      } else {
+        const float inv = 1.0f / l;
+        uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t* u = v + 8 * k;
+          srow[(4 * x + k) ^ (row & 7)] =
+              make_uint4(pack16x2<F16>(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[2]) * inv, __uint_as_float(u[3]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[6]) * inv, __uint_as_float(u[7]) * inv));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+  {
+    const int nrows = min(TQ, L - q0);
+    if constexpr (F8OUT) {
+      uint8_t* c8 = reinterpret_cast<uint8_t*>(ctx);
+      const int c = lane & 3;
+      for (int rr = warp * 8 + (lane >> 2); rr < nrows; rr += 32) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * TD)[c ^ (rr & 3)];
+        *reinterpret_cast<uint4*>(c8 + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 16) = v;
+      }
+    } else {
+      const int c = lane & 7;
+      for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
+        *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+      }
+    }
+  }
+}
+
 // ============================================================================ CLS-only last layer
 // with CLS pooling only row 0 of each request leaves the
 // last encoder layer, so its attention needs one query row per (request, head) against the
@@ -658,6 +944,10 @@ __global__ void __launch_bounds__(128) k_attention_cls(const uint16_t* __restric
 
 }  // namespace
 
+bool make_tmap_qkv64(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
+  return make_tmap_bf16_box(m, qkv, rows * static_cast<uint64_t>(3 * (H / 64)), 64, 64, 64);
+}
+
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
   // 64 bf16 = 128 B inner box (one SWIZZLE_128B row), 128 rows
   // head-major planes [3 * nh][rows][64] viewed as one [3 * nh * rows, 64] matrix: 128-token boxes of one
@@ -667,7 +957,8 @@ bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H) {
 
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st) {
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st,
+                             const CUtensorMap* tm_qkv64) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   const int d = H / num_heads;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(d));
@@ -676,6 +967,18 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
   if (d == 64) {
     if (!tm_qkv) return cudaErrorInvalidValue;
     if (f16 && ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
+    static const int engine = getenv("ELIS_ATTN_ENGINE") ? atoi(getenv("ELIS_ATTN_ENGINE")) : 64;
+    if (engine == 64 && tm_qkv64) {  // 64-key blocks, O in TMEM
+      auto kern = f16 ? k_attention_tc64<false, true> : ctx_f8_scale > 0.f ? k_attention_tc64<true, false>
+                                                                           : k_attention_tc64<false, false>;
+      if (!attr_once(reinterpret_cast<const void*>(kern))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttn64Smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<grid, 128, kAttn64Smem, st>>>(*tm_qkv64, work, num_work, H, num_heads, ctx, scale_log2,
+                                           static_cast<int>(plane_rows), ctx_f8_scale);
+      return cudaGetLastError();
+    }
     auto kern = f16 ? k_attention_tc<false, true> : ctx_f8_scale > 0.f ? k_attention_tc<true, false>
                                                                        : k_attention_tc<false, false>;
     if (!attr_once(reinterpret_cast<const void*>(kern))) {

@@ -202,7 +202,8 @@ struct elis_predictor {
   uint32_t* err = nullptr;
   int64_t max_tiles = 0;
   int tile_q = 64;          // attention q-tile rows (128 on the tcgen05 path)
-  CUtensorMap tm_qkv{};     // TMA map over qkv (tcgen05 attention)
+  CUtensorMap tm_qkv{};     // TMA maps over qkv (tcgen05 attention: 128-row / 64-row boxes)
+  CUtensorMap tm_qkv64{};
 
   // select
   int key_cap = 0;
@@ -541,7 +542,7 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   p->sc_merge.sel_keys = nullptr;
   p->sc_merge.sel_ids = nullptr;
 
-  if (H / cfg->num_heads == 64 && !make_tmap_qkv(&p->tm_qkv, p->qkv, T, H))
+  if (H / cfg->num_heads == 64 && !(make_tmap_qkv(&p->tm_qkv, p->qkv, T, H) && make_tmap_qkv64(&p->tm_qkv64, p->qkv, T, H)))
     return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled (qkv) failed");
 
   // ---- GEMM plans (TMA descriptors over the fixed workspaces; M set per call)
@@ -751,7 +752,8 @@ static elis_status predict_impl(elis_predictor* p, const int32_t* tokens, const 
     }
     LAUNCH(p, PC_ATTN, st,
            launch_attention(p->qkv, &p->tm_qkv, p->cu, p->work, p->num_work, total_tokens, n, H, c.num_heads, T_cap, p->ctx,
-                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, st));
+                            c.precision == ELIS_PREC_FP8 ? kF8ScaleCtx : 0.f, c.precision == ELIS_PREC_FP16, st,
+                            &p->tm_qkv64));
     LAUNCH(p, PC_OUT, st, launch_gemm(L.p_out, p->num_sms, st));     // + residual + LayerNorm1
     LAUNCH(p, PC_FFN1, st, launch_gemm(L.p_ffn1, p->num_sms, st));   // + GELU
     LAUNCH(p, PC_FFN2, st, launch_gemm(L.p_ffn2, p->num_sms, st));   // + residual + LayerNorm2
@@ -1523,8 +1525,9 @@ static elis_status op_attention(const uint16_t* qkv, const int32_t* lengths, int
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int tq = attn_tile_q(d);
   const int64_t tiles = attn_work_capacity(T, n, tq);
-  CUtensorMap tm{};
-  if (d == 64 && !make_tmap_qkv(&tm, qkv, static_cast<uint64_t>(T), hidden))
+  CUtensorMap tm{}, tm64{};
+  if (d == 64 && !(make_tmap_qkv(&tm, qkv, static_cast<uint64_t>(T), hidden) &&
+                   make_tmap_qkv64(&tm64, qkv, static_cast<uint64_t>(T), hidden)))
     return fail(ELIS_ERR_CUDA, "tensor map encode");
   int32_t *cu = nullptr, *nw = nullptr;
   AttnWork* work = nullptr;
@@ -1535,7 +1538,7 @@ static elis_status op_attention(const uint16_t* qkv, const int32_t* lengths, int
   CUDA_TRY(cudaMalloc(&work, tiles * sizeof(AttnWork)));
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
   CUDA_TRY(launch_meta(lengths, n, T, 512, cu, work, nw, err, tq, st));
-  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, f16, st));
+  CUDA_TRY(launch_attention(qkv, &tm, cu, work, nw, T, n, hidden, num_heads, T, ctx, 0.f, f16, st, &tm64));
   CUDA_TRY(cudaStreamSynchronize(st));
   uint32_t bits = 0;
   cudaMemcpy(&bits, err, 4, cudaMemcpyDeviceToHost);

@@ -120,13 +120,17 @@ inline int64_t attn_max_tiles(int64_t T, int n, int tile_q) { return (T + tile_q
 inline int64_t attn_work_capacity(int64_t T, int n, int tile_q) { return attn_max_tiles(T, n, tile_q); }
 // head-major qkv planes [3 * H / 64][rows][64] bf16 -> TMA map with 64-column x 128-row boxes, SWIZZLE_128B
 bool make_tmap_qkv(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
+// the same planes with 64-row boxes (the 64-key-block engine, the default; ELIS_ATTN_ENGINE=128: the
+// 128-key-block engine)
+bool make_tmap_qkv64(CUtensorMap* m, const void* qkv, uint64_t rows, int H);
 // grid: one CTA per (work item, head), head fastest, so the list's cost order is the launch order
 // head dim 64: qkv in head-major planes of plane_rows rows (tm_qkv); head dim 32: qkv [T, 3H].
 // ctx_f8_scale > 0 (head dim 64 only): ctx is written as E4M3(ctx_f8_scale * ctx) bytes [T, H];
 // f16 (head dim 64 only): qkv and ctx are fp16 instead of bf16
 cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, const int32_t* cu_seqlens,
                              const AttnWork* work, const int32_t* num_work, int64_t T, int n, int H, int num_heads,
-                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st);
+                             int64_t plane_rows, uint16_t* ctx, float ctx_f8_scale, bool f16, cudaStream_t st,
+                             const CUtensorMap* tm_qkv64 = nullptr);
 
 // CLS-only last layer: per (request, head) the attention of the CLS
 // query row (row cu[i]) over the request's keys, from the head-major qkv planes; writes the
