@@ -52,6 +52,33 @@ __device__ __forceinline__ unsigned attn_smid() {
   } while (0)
 #endif
 
+#ifdef ELIS_ATTN_TRACE
+// Diagnostic build only (python -m paper_2505_09142_b200.build --variant=atrace -DELIS_ATTN_TRACE):
+// thread 0 of every 64-key-engine CTA stamps %globaltimer (event code in the low 8 bits) at its
+// phase boundaries; scripts/attn_trace.py decodes them.
+constexpr int kTrCtas = 1 << 16, kTrEv = 48;
+__device__ unsigned long long g_attn64_trace[static_cast<size_t>(kTrCtas) * kTrEv];
+__device__ unsigned g_attn64_trace_n[kTrCtas];
+extern "C" int elis_debug_attn64_trace(unsigned long long* host, unsigned* counts) {
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_attn64_trace, sizeof(g_attn64_trace));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(counts, g_attn64_trace_n, sizeof(g_attn64_trace_n));
+  return static_cast<int>(e);
+}
+#define ATR(code)                                                                                  \
+  do {                                                                                             \
+    if (threadIdx.x == 0 && blockIdx.x < kTrCtas) {                                                \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+      if (tr_k < kTrEv) g_attn64_trace[static_cast<size_t>(blockIdx.x) * kTrEv + tr_k] = (t_ << 8) | (code); \
+      ++tr_k;                                                                                      \
+    }                                                                                              \
+  } while (0)
+#define ATR_DONE() do { if (threadIdx.x == 0 && blockIdx.x < kTrCtas) g_attn64_trace_n[blockIdx.x] = tr_k; } while (0)
+#else
+#define ATR(code) do { } while (0)
+#define ATR_DONE() do { } while (0)
+#endif
+
 namespace {
 
 constexpr int BQ = 64;          // 64 query rows per CTA (4 warps x 16)
@@ -583,8 +610,8 @@ __global__ void __launch_bounds__(128, 4)
 //                        (MMAs execute in issue order), so the next softmax waits for S only
 //   ctx = O / l          after the last block
 // No O in registers (the round-1 block of 128 keys folded O_j into 64 registers per thread, with
-// two serial TMEM passes per block).  K_{j+1} / V_{j+1} are loaded into the buffers of block
-// j - 1 as soon as S_j has completed (which implies PV_{j-1} did).  Measured (A/B, one session,
+// two serial TMEM passes per block).  Once S_j has completed, K_{j+2} is loaded into K_j's buffer
+// and V_{j+1} into V_{j-1}'s (S_j's completion implies PV_{j-1}'s).  Measured (A/B, one session,
 // profiles/r02_ab_attention_64key.txt): cfg2 attention 1.58 / 1.53 vs 1.60 / 1.54 ms per step,
 // cfg5 8.42 vs 8.58 ms; ELIS_ATTN_ENGINE=128 selects the 128-key engine above.
 constexpr int TKB64 = 64;
@@ -598,6 +625,9 @@ __global__ void __launch_bounds__(128, 4)
   const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
   const AttnWork w = work[item];
   if (item >= __ldg(num_work)) return;
+  unsigned tr_k = 0;
+  (void)tr_k;
+  ATR(1);  // start
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -606,35 +636,43 @@ __global__ void __launch_bounds__(128, 4)
   uint8_t* sV = sK + 2 * kBlk64;           // [2][64 rows]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kBlk64);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;            // [2]
-  uint64_t* s_full = bars + 3;
-  uint64_t* o_full = bars + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* k_full = bars + 1;             // [2]
+  uint64_t* v_full = bars + 3;             // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* o_full = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
 
   const int start = w.start, L = w.len, q0 = w.q0;
   const int nkb = (L + TKB64 - 1) / TKB64;  // 1..8
   const int warp = warp_id(), lane = lane_id();
   const bool issuer = threadIdx.x == 0;
   const int rq = h * Tp + start, rk = (nh + h) * Tp + start, rv = (2 * nh + h) * Tp + start;
-  auto load_kv = [&](int j) {  // block j into buffer j & 1 (64-row boxes)
-    const int b = j & 1;
-    mbar_arrive_expect_tx(&kv_full[b], 2 * kBlk64);
-    tma_load_2d(sK + b * kBlk64, &tm, &kv_full[b], 0, rk + j * TKB64);
-    tma_load_2d(sV + b * kBlk64, &tm, &kv_full[b], 0, rv + j * TKB64);
+  // K_j / V_j into buffer j & 1 (64-row boxes).  K_j is consumed by S_j, V_j only by PV_j one
+  // step later, so K is loaded two blocks ahead and V one.
+  auto load_k = [&](int j) {
+    mbar_arrive_expect_tx(&k_full[j & 1], kBlk64);
+    tma_load_2d(sK + (j & 1) * kBlk64, &tm, &k_full[j & 1], 0, rk + j * TKB64);
+  };
+  auto load_v = [&](int j) {
+    mbar_arrive_expect_tx(&v_full[j & 1], kBlk64);
+    tma_load_2d(sV + (j & 1) * kBlk64, &tm, &v_full[j & 1], 0, rv + j * TKB64);
   };
   if (issuer) {
     tma_prefetch_desc(&tm);
     mbar_init(q_full, 1);
-    mbar_init(&kv_full[0], 1);
-    mbar_init(&kv_full[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(o_full, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(q_full, kBlkBytes);
     tma_load_2d(sQ, &tm, q_full, 0, rq + q0);
     tma_load_2d(sQ + kBlk64, &tm, q_full, 0, rq + q0 + 64);
-    load_kv(0);
-    if (nkb > 1) load_kv(1);
+    load_k(0);
+    load_v(0);
+    if (nkb > 1) load_k(1);
   }
   if (warp == 1) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
@@ -647,9 +685,11 @@ __global__ void __launch_bounds__(128, 4)
   constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB64) : make_idesc_bf16_f32(TQ, TKB64);
   constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);
   const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+  ATR(2);  // setup done (barriers, TMEM)
   if (issuer) {  // S_0
     mbar_wait(q_full, 0);
-    mbar_wait(&kv_full[0], 0);
+    mbar_wait(&k_full[0], 0);
+    ATR(3);  // Q, K_0, V_0 loaded
     tc_fence_after();
     const uint64_t dk = make_sw128_desc(smem_u32(sK));
 #pragma unroll
@@ -659,10 +699,16 @@ __global__ void __launch_bounds__(128, 4)
   float m = 0.f, l = 0.f;
   const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
   for (int j = 0; j < nkb; ++j) {
+    ATR(4);  // wait S_j
     mbar_wait(s_full, j & 1);
+    ATR(5);  // S_j ready
     tc_fence_after();
-    // S_j complete => PV_{j-1} complete: the buffers of block j - 1 take block j + 1
-    if (issuer && j >= 1 && j + 1 < nkb) load_kv(j + 1);
+    // S_j complete (so K_j consumed, and PV_{j-1} complete): K_{j+2} into K_j's buffer, V_{j+1}
+    // into V_{j-1}'s
+    if (issuer) {
+      if (j + 2 < nkb) load_k(j + 2);
+      if (j + 1 < nkb) load_v(j + 1);
+    }
     const int nk = min(TKB64, L - j * TKB64);   // valid keys of this block (keys >= L: other requests)
     const int nch = (nk + 31) >> 5;             // 1..2
     if (warp_active) {
@@ -760,12 +806,15 @@ __global__ void __launch_bounds__(128, 4)
       }
       tc_wait_st();
     }
+    ATR(6);  // thread 0's softmax done
     tc_fence_before();
     __syncthreads();  // P_j complete in TMEM (all 128 rows)
+    ATR(7);  // all warps' P_j in TMEM
     if (issuer) {
       tc_fence_after();
       const int b = j & 1;
-      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      mbar_wait(&v_full[b], (j >> 1) & 1);
+      ATR(8);  // V_j (and K_j) loaded
       const int nks = (nk + 15) / 16;  // 16-key steps holding valid keys
       for (int ks = 0; ks < nks; ++ks) {
         const uint64_t dv = make_sw128_desc(smem_u32(sV + b * kBlk64 + ks * (16 * TD * 2)));
@@ -773,7 +822,7 @@ __global__ void __launch_bounds__(128, 4)
       }
       if (j + 1 < nkb) {  // S_{j+1} right behind PV_j (in issue order: P_j is read before S overwrites it)
         const int b1 = (j + 1) & 1;
-        mbar_wait(&kv_full[b1], ((j + 1) >> 1) & 1);
+        mbar_wait(&k_full[b1], ((j + 1) >> 1) & 1);
         tc_fence_after();
         const uint64_t dk = make_sw128_desc(smem_u32(sK + b1 * kBlk64));
 #pragma unroll
@@ -784,7 +833,9 @@ __global__ void __launch_bounds__(128, 4)
       }
     }
   }
+  ATR(9);  // wait last PV
   mbar_wait(o_full, 0);
+  ATR(10);  // O complete
   tc_fence_after();
   // epilogue: ctx = O / l, staged in sQ (every MMA has completed), 4 rows per warp instruction
   if (warp_active) {
@@ -847,6 +898,8 @@ __global__ void __launch_bounds__(128, 4)
       }
     }
   }
+  ATR(11);  // end
+  ATR_DONE();
 }
 
 // ============================================================================ CLS-only last layer
