@@ -12,6 +12,7 @@
 // The whole K/V of one (request, head) is <= 512 x 64 x 2 x 2 B = 128 KB.
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -353,6 +354,8 @@ __global__ void __launch_bounds__(128, 4)
 #endif
   // the work entry is read together with num_work (the list has capacity for every CTA; entries
   // past num_work are never used) and carries the request bounds: no dependent loads
+  pdl_wait();  // the work list and the qkv planes come from earlier kernels (common.cuh)
+  pdl_trigger();
   const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
   const AttnWork w = work[item];
   if (item >= __ldg(num_work)) return;
@@ -622,6 +625,8 @@ __global__ void __launch_bounds__(128, 4)
     k_attention_tc64(const __grid_constant__ CUtensorMap tm, const AttnWork* __restrict__ work,
                      const int32_t* __restrict__ num_work, int H, int nh, uint16_t* __restrict__ ctx,
                      float scale_log2, int Tp, float ctx_scale) {
+  pdl_wait();  // the work list and the qkv planes come from earlier kernels (common.cuh)
+  pdl_trigger();
   const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
   const AttnWork w = work[item];
   if (item >= __ldg(num_work)) return;
@@ -787,7 +792,9 @@ __global__ void __launch_bounds__(128, 4)
       f2_unpack(acc0, a0, a1);
       f2_unpack(acc1, a2, a3);
       l += (a0 + a1) + (a2 + a3);
-      if (resc) {  // O (complete: PV_{j-1} preceded S_j) *= alpha, before PV_j is issued
+      // O (complete: PV_{j-1} preceded S_j) *= alpha, before PV_j is issued; warp-uniform because
+      // tcgen05.ld / st are warp-collective (alpha = 1 exactly in the rows that did not rescale)
+      if (__any_sync(0xffffffffu, resc)) {
         const unsigned long long al2 = f2_pack(alpha, alpha);
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
@@ -900,6 +907,697 @@ __global__ void __launch_bounds__(128, 4)
   }
   ATR(11);  // end
   ATR_DONE();
+}
+
+// ---------------------------------------------------------------------- persistent 64-key engine
+// The 64-key engine above as a persistent kernel: 4 CTAs per SM (same 128 TMEM columns, 48 KB of
+// shared memory, thread = query row), each looping over work items c, c + G, c + 2G, ... (G = grid
+// size; the list is in descending cost order, so the stride schedule balances).  Per CTA the barrier
+// init, TMEM allocation and tensor-map prefetch happen once, and the K / V stream runs across item
+// boundaries: blocks are numbered g = 0, 1, ... over the CTA's whole sequence, K_g and V_g live in
+// buffer g & 1, and "S_g complete" (which implies PV_{g-1} complete: MMAs finish in issue order)
+// releases the loads of K_{g+2} and V_{g+1} even when those belong to the next item (only the
+// current and the next item are looked ahead; a block two items ahead waits for the next event).
+// The next item's Q is loaded once the current item's last S has completed, and its first S is
+// issued right behind the last PV, so it runs under the epilogue (O read from TMEM, ctx = O / l
+// stored straight from registers, one 128-byte row per thread).  The per-item arithmetic -- every
+// MMA, the softmax and the epilogue rounding -- is the 64-key engine's, in the same order, so
+// results are bitwise those of k_attention_tc64.
+#ifdef ELIS_ATTN_DBG
+// diagnostic build: bounded waits that report which barrier / block a persistent CTA is stuck on
+__device__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int id, int g, int it) {  // g: block, it: item
+  for (long long i = 0; i < (1ll << 22); ++i) {
+    uint32_t ok;
+    asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+  }
+  if ((threadIdx.x & 31) == 0)
+    printf("stuck: cta %d thread %d barrier %d parity %u g %d it %d\n", blockIdx.x, threadIdx.x, id, parity, g, it);
+}
+#define PWAIT(bar, par, id) mbar_wait_dbg(bar, par, id, g, it)
+#define EWAIT(bar, par, id, j) mbar_wait_dbg(bar, par, id, j, -1)
+#else
+#define EWAIT(bar, par, id, j) mbar_wait(bar, par)
+#define PWAIT(bar, par, id) mbar_wait(bar, par)
+#endif
+// ---------------------------------------------------------------------- early-S 64-key engine
+// The 64-key engine with S_{j+1} issued while softmax j runs.  In the engines above P_j overwrites
+// S_j in TMEM, so S_{j+1} can only be issued after PV_j, and every block pays PV issue + S issue +
+// S latency (~650 cycles) with its softmax warps idle -- and the 4 CTAs of an SM fall into step
+// (all in softmax, then all waiting on the shared tensor pipe).  Here P_j goes to shared memory
+// (128 rows x 64 keys, the SWIZZLE_128B K-major layout TMA gives Q, so PV_j is an SS MMA), and
+// TMEM holds only S (64 columns) and O (64 columns).  A fifth warp issues TMA and MMAs:
+//   S_{j+1}   as soon as the 4 softmax warps have read S_j into registers (s_free) and K_{j+1} landed
+//   PV_j      once P_j is in shared memory (p_full); committed to pv_done
+//   K_{j+2}   into K_j's buffer once S_{j+1} is issued (S_j completed before s_free)
+//   V_{j+1}   into V_{j-1}'s buffer once PV_{j-1} completed
+// The softmax warps wait for PV_{j-1} (pv_done) before writing P_j over P_{j-1} and before a lazy
+// O rescale.  64 KB of shared memory and 160 threads: 3 CTAs per SM.  Per-block arithmetic (MMA
+// shapes and order, softmax, P rounding, epilogue) is the 64-key engine's, so results are bitwise
+// those of k_attention_tc64.
+constexpr int kAttnESmem = kBlkBytes + 4 * kBlk64 + kBlkBytes + 1024 + 256;  // Q, K[2], V[2], P
+template <bool F8OUT, bool F16>
+__global__ void __launch_bounds__(160, 3)
+    k_attention_tc64e(const __grid_constant__ CUtensorMap tm, const AttnWork* __restrict__ work,
+                      const int32_t* __restrict__ num_work, int H, int nh, uint16_t* __restrict__ ctx,
+                      float scale_log2, int Tp, float ctx_scale) {
+  pdl_wait();  // the work list and the qkv planes come from earlier kernels (common.cuh)
+  pdl_trigger();
+  const int item = static_cast<int>(blockIdx.x) / nh, h = static_cast<int>(blockIdx.x) % nh;
+  const AttnWork w = work[item];
+  if (item >= __ldg(num_work)) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* sQ = smem;                      // 128 rows
+  uint8_t* sK = sQ + kBlkBytes;            // [2][64 rows]
+  uint8_t* sV = sK + 2 * kBlk64;           // [2][64 rows]
+  uint8_t* sP = sV + 2 * kBlk64;           // 128 rows x 64 keys, SWIZZLE_128B K-major
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kBlkBytes);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;             // [2]
+  uint64_t* v_full = bars + 3;             // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* s_free = bars + 6;             // 4 arrivals: S_j read by every softmax warp
+  uint64_t* p_full = bars + 7;             // 4 arrivals: P_j written by every softmax warp
+  uint64_t* pv_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int start = w.start, L = w.len, q0 = w.q0;
+  const int nkb = (L + TKB64 - 1) / TKB64;  // 1..8
+  const int warp = warp_id(), lane = lane_id();
+  const bool issuer = threadIdx.x == 128;   // warp 4, lane 0
+  const int rq = h * Tp + start, rk = (nh + h) * Tp + start, rv = (2 * nh + h) * Tp + start;
+  auto load_k = [&](int j) {
+    mbar_arrive_expect_tx(&k_full[j & 1], kBlk64);
+    tma_load_2d(sK + (j & 1) * kBlk64, &tm, &k_full[j & 1], 0, rk + j * TKB64);
+  };
+  auto load_v = [&](int j) {
+    mbar_arrive_expect_tx(&v_full[j & 1], kBlk64);
+    tma_load_2d(sV + (j & 1) * kBlk64, &tm, &v_full[j & 1], 0, rv + j * TKB64);
+  };
+  if (issuer) {
+    tma_prefetch_desc(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(q_full, kBlkBytes);
+    tma_load_2d(sQ, &tm, q_full, 0, rq + q0);
+    tma_load_2d(sQ + kBlk64, &tm, q_full, 0, rq + q0 + 64);
+    load_k(0);
+    load_v(0);
+    if (nkb > 1) {
+      load_k(1);
+      load_v(1);
+    }
+  }
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB64) : make_idesc_bf16_f32(TQ, TKB64);
+  constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);
+
+  float m = 0.f, l = 0.f;  // softmax warps: running row max (log2 units) and row sum
+  if (warp == 4) {
+    // ------------------------------------------------ TMA + MMA issuer
+    if (issuer) {
+      const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+      const uint64_t dp = make_sw128_desc(smem_u32(sP));
+      auto issue_s = [&](int j) {
+        const int b = j & 1;
+        EWAIT(&k_full[b], (j >> 1) & 1, 1, j);
+        tc_fence_after();
+        const uint64_t dk = make_sw128_desc(smem_u32(sK + b * kBlk64));
+#pragma unroll
+        for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+        tc_commit(s_full);
+      };
+      EWAIT(q_full, 0, 0, 0);
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        if (j + 1 < nkb) {
+          EWAIT(s_free, j & 1, 7, j);  // S_j is in the softmax warps' registers (and S_j completed)
+          tc_fence_after();
+          issue_s(j + 1);
+          if (j + 2 < nkb) load_k(j + 2);  // K_j consumed by S_j
+          if (j >= 1) {                    // V_{j+1} over V_{j-1}: PV_{j-1} must have completed
+            EWAIT(pv_done, (j - 1) & 1, 9, j);
+            load_v(j + 1);
+          }
+        }
+        const int nk = min(TKB64, L - j * TKB64);
+        const int b = j & 1;
+        EWAIT(p_full, j & 1, 8, j);
+        EWAIT(&v_full[b], (j >> 1) & 1, 3, j);
+        tc_fence_after();
+        const int nks = (nk + 15) / 16;
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t dv = make_sw128_desc(smem_u32(sV + b * kBlk64 + ks * (16 * TD * 2)));
+          tc_mma_f16(tmem + kOCol, dp + 2 * ks, dv, idesc_o, (j | ks) != 0 ? 1u : 0u);
+        }
+        tc_commit(pv_done);
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax warps (thread = query row)
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int row = warp * 32 + lane;
+    const bool warp_active = q0 + warp * 32 < L;
+    uint8_t* prow = sP + row * 128;
+    const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
+    for (int j = 0; j < nkb; ++j) {
+      const int nk = min(TKB64, L - j * TKB64);
+      const int nch = (nk + 31) >> 5;
+      if (!warp_active) {
+        // rows all beyond L: nothing to compute, but s_free / p_full count 4 warps, and an arrival
+        // lands in the barrier's current phase -- so arrive only once that phase is the block's own
+        // (S_j issued implies s_free phase j-1 complete; PV_{j-1} complete implies p_full phase j-1)
+        EWAIT(s_full, j & 1, 15, j);
+        if (lane == 0) mbar_arrive(s_free);
+        __syncwarp();  // reconverge before the next spin loop (the arriving lane must not be starved)
+        if (j > 0) EWAIT(pv_done, (j - 1) & 1, 19, j);
+        if (lane == 0) mbar_arrive(p_full);
+        __syncwarp();
+        continue;
+      }
+      {
+        uint32_t r[2][32];
+        EWAIT(s_full, j & 1, 5, j);
+        tc_fence_after();
+        tmem_ld_32x32b_x32(taddr, r[0]);
+        if (nch > 1) tmem_ld_32x32b_x32(taddr + 32, r[1]);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);  // S_j may now be overwritten by S_{j+1}
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch && nk < 32 * (c + 1)) {
+            const int tail = nk - 32 * c;
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e >= tail) r[c][e] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(r[0][i]);
+#pragma unroll
+        for (int e = 8; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[0][e]), __uint_as_float(r[0][e + 1]));
+        if (nch > 1) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[1][e]), __uint_as_float(r[1][e + 1]));
+        }
+        const float bm = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+        const float ms = bm * scale_log2;
+        float alpha = 1.f;
+        bool resc = false;
+        if (j == 0) {
+          m = ms;
+        } else if (ms > m + kLazyRescale) {
+          alpha = ex2_approx(m - ms);
+          m = ms;
+          l *= alpha;
+          resc = true;
+        }
+        const unsigned long long nm2 = f2_pack(-m, -m);
+        unsigned long long acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
+        uint32_t pk[2][16];  // P_j as 16-bit pairs
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float x0, x1, p0, p1;
+              f2_unpack(f2_fma(f2_pack(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1])), sc2, nm2), x0, x1);
+              if (exp2_on_fma(e)) {
+                f2_unpack(exp2_poly2(x0, x1), p0, p1);
+              } else {
+                p0 = ex2_approx(x0);
+                p1 = ex2_approx(x1);
+              }
+              r[c][2 * e] = __float_as_uint(p0);
+              r[c][2 * e + 1] = __float_as_uint(p1);
+            }
+            if (nk < 32 * (c + 1)) {
+              const int tail = nk - 32 * c;
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (e >= tail) r[c][e] = 0u;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              acc0 = f2_add(acc0, f2_pack(__uint_as_float(r[c][4 * e]), __uint_as_float(r[c][4 * e + 1])));
+              acc1 = f2_add(acc1, f2_pack(__uint_as_float(r[c][4 * e + 2]), __uint_as_float(r[c][4 * e + 3])));
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[c][e] = pack16x2<F16>(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]));
+          }
+        }
+        float a0, a1, a2, a3;
+        f2_unpack(acc0, a0, a1);
+        f2_unpack(acc1, a2, a3);
+        l += (a0 + a1) + (a2 + a3);
+        // PV_{j-1} must have completed: it reads P_{j-1} (overwritten below) and accumulates into O
+        if (j > 0) {
+          EWAIT(pv_done, (j - 1) & 1, 29, j);
+          tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, resc)) {  // warp-uniform (tcgen05.ld / st); alpha = 1 where !resc
+          const unsigned long long al2 = f2_pack(alpha, alpha);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(taddr + kOCol + x * 32, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float o0, o1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])), al2), o0, o1);
+              o[2 * i] = __float_as_uint(o0);
+              o[2 * i + 1] = __float_as_uint(o1);
+            }
+            tmem_st_32x32b_x32(taddr + kOCol + x * 32, o);
+          }
+          tc_wait_st();
+        }
+        // P_j row -> shared memory: 16-byte chunk c of the 128-byte row at chunk c ^ (row & 7)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int chunk = 4 * c + q;
+              *reinterpret_cast<uint4*>(prow + 16 * (chunk ^ (row & 7))) =
+                  make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+            }
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy P stores -> the MMA's async-proxy reads
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        __syncwarp();
+      }
+    }
+  }
+  // epilogue: ctx = O / l once the last PV has completed (every MMA has: sQ is free), rows staged in
+  // sQ with 16-byte chunks XOR-swizzled by row, then written back 4 rows per warp instruction
+  const int row = warp * 32 + lane;
+  if (warp < 4 && q0 + warp * 32 < L) {
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    EWAIT(pv_done, (nkb - 1) & 1, 39, nkb);
+    tc_fence_after();
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr + kOCol + x * 32, v);
+      tc_wait_ld();
+      if constexpr (F8OUT) {
+        const float inv = ctx_scale / l;
+        uint4* srow = reinterpret_cast<uint4*>(sQ + row * TD);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t* u = v + 16 * k;
+          srow[(2 * x + k) ^ (row & 3)] = make_uint4(
+              pack_e4m3x4(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv, __uint_as_float(u[2]) * inv,
+                          __uint_as_float(u[3]) * inv),
+              pack_e4m3x4(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv, __uint_as_float(u[6]) * inv,
+                          __uint_as_float(u[7]) * inv),
+              pack_e4m3x4(__uint_as_float(u[8]) * inv, __uint_as_float(u[9]) * inv, __uint_as_float(u[10]) * inv,
+                          __uint_as_float(u[11]) * inv),
+              pack_e4m3x4(__uint_as_float(u[12]) * inv, __uint_as_float(u[13]) * inv, __uint_as_float(u[14]) * inv,
+                          __uint_as_float(u[15]) * inv));
+        }
+      } else {
+        const float inv = 1.0f / l;
+        uint4* srow = reinterpret_cast<uint4*>(sQ + row * (TD * 2));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t* u = v + 8 * k;
+          srow[(4 * x + k) ^ (row & 7)] =
+              make_uint4(pack16x2<F16>(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[2]) * inv, __uint_as_float(u[3]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv),
+                         pack16x2<F16>(__uint_as_float(u[6]) * inv, __uint_as_float(u[7]) * inv));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
+  if (warp < 4) {
+    const int nrows = min(TQ, L - q0);
+    if constexpr (F8OUT) {
+      uint8_t* c8 = reinterpret_cast<uint8_t*>(ctx);
+      const int c = lane & 3;
+      for (int rr = warp * 8 + (lane >> 2); rr < nrows; rr += 32) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * TD)[c ^ (rr & 3)];
+        *reinterpret_cast<uint4*>(c8 + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 16) = v;
+      }
+    } else {
+      const int c = lane & 7;
+      for (int rr = warp * 4 + (lane >> 3); rr < nrows; rr += 16) {
+        const uint4 v = reinterpret_cast<const uint4*>(sQ + rr * (TD * 2))[c ^ (rr & 7)];
+        *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(start + q0 + rr) * H + h * TD + c * 8) = v;
+      }
+    }
+  }
+}
+
+struct AttnItem {
+  int start, L, q0, h, nkb;
+};
+struct IssuerState {
+  AttnItem cur, nxt;  // the items K / V loads may target
+  AttnWork nn;        // the item after nxt, fetched one item early
+  int gbase, nk, nv;  // global index of cur's block 0; K / V blocks issued so far
+};
+static_assert(8 * 8 + sizeof(IssuerState) + 2 * sizeof(AttnItem) <= 256, "persistent engine smem tail");
+template <bool F8OUT, bool F16>
+__global__ void __launch_bounds__(128, 4)
+    k_attention_tc64p(const __grid_constant__ CUtensorMap tm, const AttnWork* __restrict__ work,
+                      const int32_t* __restrict__ num_work, int H, int nh, uint16_t* __restrict__ ctx,
+                      float scale_log2, int Tp, float ctx_scale) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* sQ = smem;                      // 128 rows
+  uint8_t* sK = sQ + kBlkBytes;            // [2][64 rows]
+  uint8_t* sV = sK + 2 * kBlk64;           // [2][64 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kBlk64);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;             // [2]
+  uint64_t* v_full = bars + 3;             // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* o_full = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  const int warp = warp_id(), lane = lane_id();
+  const bool issuer = threadIdx.x == 0;
+  if (issuer) {
+    tma_prefetch_desc(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int row = warp * 32 + lane;
+  constexpr uint32_t idesc_s = F16 ? make_idesc_f16_f32(TQ, TKB64) : make_idesc_bf16_f32(TQ, TKB64);
+  constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);
+  const uint64_t dq = make_sw128_desc(smem_u32(sQ));
+
+  pdl_wait();  // the work list and the qkv planes come from earlier kernels (common.cuh)
+  pdl_trigger();
+  const int total = __ldg(num_work) * nh;  // (work item, head) pairs
+  const int G = static_cast<int>(gridDim.x);
+  // The issuer's look-ahead state lives in shared memory (thread 0 only), so that it is not live
+  // in registers across the softmax; every thread reads the next item from islot[] at the item
+  // boundary (written by thread 0 before the item's first block barrier).
+  IssuerState* ist = reinterpret_cast<IssuerState*>(bars + 8);
+  AttnItem* islot = reinterpret_cast<AttnItem*>(ist + 1);  // [2]: item k in slot k & 1
+  auto decode = [&](int i, const AttnWork& w) -> AttnItem {
+    if (i >= total) return AttnItem{0, 0, 0, 0, 0};
+    return AttnItem{w.start, w.len, w.q0, i % nh, (w.len + TKB64 - 1) / TKB64};
+  };
+  auto fetch = [&](int i) -> AttnWork { return i < total ? work[i / nh] : AttnWork{0, 0, 0, 0}; };
+  int it = static_cast<int>(blockIdx.x);
+  AttnItem cur = decode(it, fetch(it));
+  uint32_t items_done = 0;
+  int g = 0;  // global block index over the CTA's sequence
+  // at "S_g complete" (g = -1 before the first S): K up to g + 2, V up to g + 1, over cur and nxt
+  auto issue_loads = [&](int g) {
+    const AttnItem c = ist->cur, n = ist->nxt;
+    const int gb = ist->gbase;
+    auto blk_row = [&](int mb, int plane, int& r) -> bool {
+      int rel = mb - gb;
+      if (rel < c.nkb) {
+        r = (plane * nh + c.h) * Tp + c.start + rel * TKB64;
+        return true;
+      }
+      rel -= c.nkb;
+      if (rel < n.nkb) {
+        r = (plane * nh + n.h) * Tp + n.start + rel * TKB64;
+        return true;
+      }
+      return false;
+    };
+    int r, nk = ist->nk, nv = ist->nv;
+    while (nk <= g + 2 && blk_row(nk, 1, r)) {
+      mbar_arrive_expect_tx(&k_full[nk & 1], kBlk64);
+      tma_load_2d(sK + (nk & 1) * kBlk64, &tm, &k_full[nk & 1], 0, r);
+      ++nk;
+    }
+    while (nv <= g + 1 && blk_row(nv, 2, r)) {
+      mbar_arrive_expect_tx(&v_full[nv & 1], kBlk64);
+      tma_load_2d(sV + (nv & 1) * kBlk64, &tm, &v_full[nv & 1], 0, r);
+      ++nv;
+    }
+    ist->nk = nk;
+    ist->nv = nv;
+  };
+  auto load_q = [&](const AttnItem& x) {
+    const int r = x.h * Tp + x.start + x.q0;
+    mbar_arrive_expect_tx(q_full, kBlkBytes);
+    tma_load_2d(sQ, &tm, q_full, 0, r);
+    tma_load_2d(sQ + kBlk64, &tm, q_full, 0, r + 64);
+  };
+  auto issue_s = [&](int gnext) {  // S_gnext = Q K_gnext^T into columns [0, 64)
+    const int b = gnext & 1;
+    PWAIT(&k_full[b], (gnext >> 1) & 1, 1);
+    tc_fence_after();
+    const uint64_t dk = make_sw128_desc(smem_u32(sK + b * kBlk64));
+#pragma unroll
+    for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+    tc_commit(s_full);
+  };
+  if (issuer) {
+    ist->cur = cur;
+    ist->nxt = decode(it + G, fetch(it + G));
+    ist->nn = fetch(it + 2 * G);
+    ist->gbase = 0;
+    ist->nk = 0;
+    ist->nv = 0;
+    if (cur.nkb > 0) {
+      load_q(cur);
+      issue_loads(-1);
+      PWAIT(q_full, 0, 0);
+      issue_s(0);
+    }
+  }
+
+  const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
+  while (it < total) {
+    const int L = cur.L, q0 = cur.q0, nkb = cur.nkb;
+    const bool warp_active = q0 + warp * 32 < L;
+    float m = 0.f, l = 0.f;
+    for (int j = 0; j < nkb; ++j, ++g) {
+      PWAIT(s_full, g & 1, 5);
+      tc_fence_after();
+      if (issuer) {
+        if (j == 0) islot[(items_done + 1) & 1] = ist->nxt;  // read by every thread at the item boundary
+        if (j == nkb - 1 && ist->nxt.nkb > 0) load_q(ist->nxt);  // the last S of this item has read Q
+        issue_loads(g);
+      }
+      const int nk = min(TKB64, L - j * TKB64);
+      const int nch = (nk + 31) >> 5;
+      if (warp_active) {
+        uint32_t r[2][32];
+        tmem_ld_32x32b_x32(taddr, r[0]);
+        if (nch > 1) tmem_ld_32x32b_x32(taddr + 32, r[1]);
+        tc_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch && nk < 32 * (c + 1)) {
+            const int tail = nk - 32 * c;
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (e >= tail) r[c][e] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = __uint_as_float(r[0][i]);
+#pragma unroll
+        for (int e = 8; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[0][e]), __uint_as_float(r[0][e + 1]));
+        if (nch > 1) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) mx[(e >> 1) & 7] = fmax3(mx[(e >> 1) & 7], __uint_as_float(r[1][e]), __uint_as_float(r[1][e + 1]));
+        }
+        const float bm = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmax3(fmax3(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+        const float ms = bm * scale_log2;
+        float alpha = 1.f;
+        bool resc = false;
+        if (j == 0) {
+          m = ms;
+        } else if (ms > m + kLazyRescale) {
+          alpha = ex2_approx(m - ms);
+          m = ms;
+          l *= alpha;
+          resc = true;
+        }
+        const unsigned long long nm2 = f2_pack(-m, -m);
+        unsigned long long acc0 = f2_pack(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float x0, x1, p0, p1;
+              f2_unpack(f2_fma(f2_pack(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1])), sc2, nm2), x0, x1);
+              if (exp2_on_fma(e)) {
+                f2_unpack(exp2_poly2(x0, x1), p0, p1);
+              } else {
+                p0 = ex2_approx(x0);
+                p1 = ex2_approx(x1);
+              }
+              r[c][2 * e] = __float_as_uint(p0);
+              r[c][2 * e + 1] = __float_as_uint(p1);
+            }
+            if (nk < 32 * (c + 1)) {
+              const int tail = nk - 32 * c;
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (e >= tail) r[c][e] = 0u;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              acc0 = f2_add(acc0, f2_pack(__uint_as_float(r[c][4 * e]), __uint_as_float(r[c][4 * e + 1])));
+              acc1 = f2_add(acc1, f2_pack(__uint_as_float(r[c][4 * e + 2]), __uint_as_float(r[c][4 * e + 3])));
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = pack16x2<F16>(__uint_as_float(r[c][2 * e]), __uint_as_float(r[c][2 * e + 1]));
+            tmem_st_32x32b_x16(taddr + c * 16, pk);
+          }
+        }
+        float a0, a1, a2, a3;
+        f2_unpack(acc0, a0, a1);
+        f2_unpack(acc1, a2, a3);
+        l += (a0 + a1) + (a2 + a3);
+        if (__any_sync(0xffffffffu, resc)) {  // warp-uniform (tcgen05.ld / st); alpha = 1 where !resc
+          const unsigned long long al2 = f2_pack(alpha, alpha);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(taddr + kOCol + x * 32, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float o0, o1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1])), al2), o0, o1);
+              o[2 * i] = __float_as_uint(o0);
+              o[2 * i + 1] = __float_as_uint(o1);
+            }
+            tmem_st_32x32b_x32(taddr + kOCol + x * 32, o);
+          }
+        }
+        tc_wait_st();
+      }
+      tc_fence_before();
+      __syncthreads();  // P_g complete in TMEM (all 128 rows); the previous item's O has been read
+      if (issuer) {
+        tc_fence_after();
+        const int b = g & 1;
+        PWAIT(&v_full[b], (g >> 1) & 1, 3);
+        const int nks = (nk + 15) / 16;
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t dv = make_sw128_desc(smem_u32(sV + b * kBlk64 + ks * (16 * TD * 2)));
+          tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, (j | ks) != 0 ? 1u : 0u);
+        }
+        if (j + 1 < nkb) {
+          issue_s(g + 1);
+        } else {
+          tc_commit(o_full);
+          if (ist->nxt.nkb > 0) {  // the next item's first S runs under this item's epilogue
+            PWAIT(q_full, (items_done + 1) & 1, 10);
+            issue_s(g + 1);
+          }
+        }
+      }
+    }
+    PWAIT(o_full, items_done & 1, 6);
+    tc_fence_after();
+    // epilogue: ctx = O / l, one row per thread straight from registers
+    if (warp_active) {  // tcgen05.ld is warp-collective: whole warps load, rows < L store
+      const bool store = q0 + row < L;
+      const int h = cur.h;
+      const size_t grow = static_cast<size_t>(cur.start + q0 + row);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(taddr + kOCol + x * 32, v);
+        tc_wait_ld();
+        if constexpr (F8OUT) {
+          const float inv = ctx_scale / l;
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(ctx) + grow * H + h * TD + x * 32);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uint32_t* u = v + 16 * k;
+            if (store) dst[k] = make_uint4(
+                pack_e4m3x4(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv, __uint_as_float(u[2]) * inv,
+                            __uint_as_float(u[3]) * inv),
+                pack_e4m3x4(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv, __uint_as_float(u[6]) * inv,
+                            __uint_as_float(u[7]) * inv),
+                pack_e4m3x4(__uint_as_float(u[8]) * inv, __uint_as_float(u[9]) * inv, __uint_as_float(u[10]) * inv,
+                            __uint_as_float(u[11]) * inv),
+                pack_e4m3x4(__uint_as_float(u[12]) * inv, __uint_as_float(u[13]) * inv, __uint_as_float(u[14]) * inv,
+                            __uint_as_float(u[15]) * inv));
+          }
+        } else {
+          const float inv = 1.0f / l;
+          uint4* dst = reinterpret_cast<uint4*>(ctx + grow * H + h * TD + x * 32);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t* u = v + 8 * k;
+            if (store) dst[k] = make_uint4(pack16x2<F16>(__uint_as_float(u[0]) * inv, __uint_as_float(u[1]) * inv),
+                                pack16x2<F16>(__uint_as_float(u[2]) * inv, __uint_as_float(u[3]) * inv),
+                                pack16x2<F16>(__uint_as_float(u[4]) * inv, __uint_as_float(u[5]) * inv),
+                                pack16x2<F16>(__uint_as_float(u[6]) * inv, __uint_as_float(u[7]) * inv));
+          }
+        }
+      }
+    }
+    it += G;
+    if (issuer) {  // advance the look-ahead: cur <- nxt <- nn
+      ist->gbase += nkb;
+      ist->cur = ist->nxt;
+      ist->nxt = decode(it + G, ist->nn);
+      ist->nn = fetch(it + 2 * G);
+    }
+    cur = islot[(items_done + 1) & 1];
+    ++items_done;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<128>(tmem);
+  }
 }
 
 // ============================================================================ CLS-only last layer
@@ -1021,6 +1719,52 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
     if (!tm_qkv) return cudaErrorInvalidValue;
     if (f16 && ctx_f8_scale > 0.f) return cudaErrorInvalidValue;
     static const int engine = getenv("ELIS_ATTN_ENGINE") ? atoi(getenv("ELIS_ATTN_ENGINE")) : 64;
+    if (engine == 65 && tm_qkv64) {  // persistent 64-key engine: 4 CTAs per SM loop over the items
+      auto kern = f16 ? k_attention_tc64p<false, true> : ctx_f8_scale > 0.f ? k_attention_tc64p<true, false>
+                                                                            : k_attention_tc64p<false, false>;
+      if (!attr_once(reinterpret_cast<const void*>(kern))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttn64Smem);
+        if (e != cudaSuccess) return e;
+      }
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const unsigned pgrid = std::min<unsigned>(grid, 4u * static_cast<unsigned>(sms));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(pgrid);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = kAttn64Smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      pdl_attr(attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *tm_qkv64, work, num_work, H, num_heads, ctx, scale_log2,
+                                         static_cast<int>(plane_rows), ctx_f8_scale);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
+    if (engine == 66 && tm_qkv64) {  // early-S 64-key engine: P in shared memory, issuer warp
+      auto kern = f16 ? k_attention_tc64e<false, true> : ctx_f8_scale > 0.f ? k_attention_tc64e<true, false>
+                                                                            : k_attention_tc64e<false, false>;
+      if (!attr_once(reinterpret_cast<const void*>(kern))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnESmem);
+        if (e != cudaSuccess) return e;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(160);
+      cfg.dynamicSmemBytes = kAttnESmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      pdl_attr(attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *tm_qkv64, work, num_work, H, num_heads, ctx, scale_log2,
+                                         static_cast<int>(plane_rows), ctx_f8_scale);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
     if (engine == 64 && tm_qkv64) {  // 64-key blocks, O in TMEM
       auto kern = f16 ? k_attention_tc64<false, true> : ctx_f8_scale > 0.f ? k_attention_tc64<true, false>
                                                                            : k_attention_tc64<false, false>;
@@ -1028,8 +1772,18 @@ cudaError_t launch_attention(const uint16_t* qkv, const CUtensorMap* tm_qkv, con
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttn64Smem);
         if (e != cudaSuccess) return e;
       }
-      kern<<<grid, 128, kAttn64Smem, st>>>(*tm_qkv64, work, num_work, H, num_heads, ctx, scale_log2,
-                                           static_cast<int>(plane_rows), ctx_f8_scale);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = kAttn64Smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      pdl_attr(attr[0]);
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *tm_qkv64, work, num_work, H, num_heads, ctx, scale_log2,
+                                         static_cast<int>(plane_rows), ctx_f8_scale);
+      if (e != cudaSuccess) return e;
       return cudaGetLastError();
     }
     auto kern = f16 ? k_attention_tc<false, true> : ctx_f8_scale > 0.f ? k_attention_tc<true, false>

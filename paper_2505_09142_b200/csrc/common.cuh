@@ -416,4 +416,27 @@ inline bool attr_once(const void* fn) {
   return !done.insert({fn, dev}).second;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The layer chain's tensor-core kernels (GEMMs, attention) are launched with programmatic stream
+// serialization: kernel i+1's CTAs may be scheduled (and run their prologue -- barrier init, TMEM
+// allocation, tensor-map prefetch) while kernel i drains its last wave.  Every such kernel runs
+// pdl_wait() before its first access to memory an earlier kernel writes (griddepcontrol.wait returns
+// once the whole preceding grid has completed and its writes are visible; a no-op without the launch
+// attribute), and pdl_trigger() only after it, so a dependent's pre-wait code overlaps at most the
+// immediately preceding kernel -- which has itself passed its wait, i.e. everything earlier is done.
+ELIS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ELIS_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Host: whether to launch the chain kernels with the attribute (ELIS_PDL=0 disables, for A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ELIS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline void pdl_attr(cudaLaunchAttribute& a) {
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+}
+
 }  // namespace elis

@@ -251,9 +251,7 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int M = args.M_dev ? min(max(__ldg(args.M_dev), 0), args.M) : args.M;
   const int N = args.N, K = args.K;
-  const int num_m = (M + 2 * BM - 1) / (2 * BM);  // 256-row pair tiles
   const int num_n = N / BN;
   const int num_k = K / BKE;
   // Cluster = (LN ? num_n : 1) pairs.  CTA rank r: pair r >> 1, half (row half / B half) r & 1.
@@ -266,11 +264,6 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
   const int leader_rank = crank & ~1;
   const int cid = static_cast<int>(blockIdx.x) / (2 * cpairs);
   const int ncl = static_cast<int>(gridDim.x) / (2 * cpairs);
-  const int num_iter_tiles = LNC ? num_m : num_m * num_n;
-  auto tile_mn = [&](int t, int& m, int& n) {
-    if (LNC) { m = t; n = pair_in_cluster; } else { m = t / num_n; n = t % num_n; }
-    if (args.m_reverse) m = num_m - 1 - m;
-  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -296,6 +289,17 @@ __global__ void __launch_bounds__(gemm_threads<EPI, PREC>(), 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above touches only this kernel's parameters; the row count and every operand below
+  // may come from the preceding kernel (programmatic dependent launch, common.cuh)
+  pdl_wait();
+  pdl_trigger();
+  const int M = args.M_dev ? min(max(__ldg(args.M_dev), 0), args.M) : args.M;
+  const int num_m = (M + 2 * BM - 1) / (2 * BM);  // 256-row pair tiles
+  const int num_iter_tiles = LNC ? num_m : num_m * num_n;
+  auto tile_mn = [&](int t, int& m, int& n) {
+    if (LNC) { m = t; n = pair_in_cluster; } else { m = t / num_n; n = t % num_n; }
+    if (args.m_reverse) m = num_m - 1 - m;
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs); bytes counted on the leader's full barrier
@@ -723,13 +727,14 @@ cudaError_t launch_bn(const GemmPlan& g, int num_sms, cudaStream_t st) {
   cfg.blockDim = dim3(gemm_threads<EPI, PREC>());
   cfg.dynamicSmemBytes = SP::SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  pdl_attr(attr[1]);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl_enabled() && !GX) ? 2 : 1;  // GX spins on the whole grid being co-resident
   if (first && csize > 8) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--cap", type=int, default=256)
     ap.add_argument("--pooling", default="mean", choices=["mean", "cls"])
     ap.add_argument("--cls-last-layer", action="store_true", help="CLS pooling: last layer on CLS rows only")
+    ap.add_argument("--dump", default=None, help="save predictions + final hidden states (.npz) for bitwise A/B")
     ap.add_argument("--residual", default=None, choices=["fp16", "fp32"], help="residual stream (default: the library's)")
     a = ap.parse_args()
     cfg = inputs.CONFIGS[a.config]
@@ -81,6 +82,12 @@ def main():
     if a.time:
         prof = p.profile_read()
         print({k: round(ms / a.iters, 4) for k, (ms, _) in prof.items()})
+    if a.dump:
+        hid = torch.empty(T * cfg.hidden, dtype=torch.float32, device=dev)
+        p.get_hidden(hid)
+        torch.cuda.synchronize()
+        pred = out if slots is None else table[torch.from_numpy(slots).to(dev)]
+        np.savez(a.dump, pred=pred.cpu().numpy(), hidden=hid.cpu().numpy())
     print(f"T={T} n={a.n} pred[0:4]={(out if slots is None else table[torch.from_numpy(slots[:4]).to(dev)])[:4].tolist()}")
 
 

@@ -192,6 +192,38 @@ def test_attention_batch_invariant_across_packs(cuda_lib, f16):
             assert torch.equal(got.view(torch.int16), alone[i].view(torch.int16)), (prefix, int(probe[i]))
 
 
+@pytest.mark.parametrize("f16", [False, True])
+def test_attention_lazy_rescale(cuda_lib, f16):
+    """Keys whose magnitude grows along the request (x6 from key 64, x12 from key 192), so the block
+    maximum of later 64-key blocks exceeds the running maximum by more than 2^8, except in every third
+    query row (scaled to near-flat scores): the lazy O rescale runs for part of a warp's rows (warp-uniform TMEM access, alpha = 1
+    in the other rows).  Every request vs the fp64 oracle."""
+    from paper_2505_09142_b200 import binding
+    from oracle import encoder as oenc
+    H, nh = 768, 12
+    rng = np.random.default_rng(11)
+    lengths = np.array([100, 300, 512, 65, 200, 129], np.int32)
+    T = int(lengths.sum())
+    x = rng.normal(0, 1.0, (T, 3 * H))
+    starts = inputs.offsets(lengths)
+    for i, L in enumerate(lengths):
+        pos = np.arange(L)
+        scale = np.where(pos >= 192, 12.0, np.where(pos >= 64, 6.0, 1.0))
+        x[starts[i]:starts[i + 1], H:2 * H] *= scale[:, None]
+        x[starts[i]:starts[i + 1]:3, :H] *= 0.01  # every third query row: flat scores, no rescale
+    qkv, qkv64 = fp16_tensor(x) if f16 else bf16_tensor(x)
+    ctx = torch.full((T, H), float("nan"), dtype=torch.float16 if f16 else torch.bfloat16, device="cuda")
+    binding.op_attention(attn_layout(qkv, H, nh), torch.from_numpy(lengths).cuda(), H, nh, ctx, f16=f16)
+    torch.cuda.synchronize()
+    got = to_np(ctx)
+    tol = 4e-3 if f16 else 2e-2
+    for i, L in enumerate(lengths):
+        sl = slice(starts[i], starts[i + 1])
+        ref = oenc.attention(qkv64[sl, :H], qkv64[sl, H:2 * H], qkv64[sl, 2 * H:], nh)
+        err = np.abs(got[sl] - ref).max()
+        assert err < tol, (i, int(L), err)
+
+
 def test_attention_single_token_is_v(cuda_lib):
     """L = 1 closed form on the GPU: ctx = v (up to bf16 of a bf16 value: exact)."""
     from paper_2505_09142_b200 import binding
