@@ -104,3 +104,77 @@ def test_bench_reference_arm_runs_on_cpu(tmp_path):
     assert line["impl"] == "reference" and line["value"] > 0
     for k in ("cpu_baseline", "e2e", "metric", "unit", "config"):
         assert k in line
+
+
+def _shard_worker(rank, world, port, win, out_q):
+    """One rank of bench.py's cfg5 multi-GPU iteration, host side: the due window is split at the
+    quantiles of its encoder cost by the LIBRARY (elis_cost_split, a host function of the C ABI),
+    each rank writes predictions for its slice only, the (slot, prediction) pairs are all-gathered
+    into every rank's copy of the 65,536-slot table, and every rank selects over the whole table."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from oracle.select import isrtf_select
+    cfg = inputs.CONFIGS["base"]
+    F, due = 65536, -(-65536 // inputs.WINDOW_K)
+    Lt = np.asarray(inputs.trace_lengths(F, seed=0)[0], np.int32)
+    slots = bench.due_windows(F, due)[win]
+    b = bench.cost_bounds(Lt[slots], world, cfg)
+    mine = slots[b[rank]:b[rank + 1]]
+    # stand-in for this rank's encoder output: any deterministic function of the slot
+    pred_all = inputs.random_predictions(F, seed=win)
+    table = np.zeros(F, np.float32)
+    pairs = np.full((due, 2), -1.0, np.float64)
+    pairs[:len(mine), 0] = mine
+    pairs[:len(mine), 1] = pred_all[mine]
+    t = torch.from_numpy(pairs)
+    gathered = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(gathered, t)
+    for g in gathered:
+        g = g.numpy()
+        g = g[g[:, 0] >= 0]
+        table[g[:, 0].astype(np.int64)] = g[:, 1].astype(np.float32)
+    gen, order, running = inputs.random_sched_state(F, seed=win)
+    ids, cnt, _, _ = isrtf_select(table, gen, 256, 0, True, order, running)
+    out_q.put((rank, [int(x) for x in b], mine.tolist(), ids[:cnt].tolist(), table[slots].tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,win", [(2, 0), (4, 7)])
+def test_cfg5_due_set_sharding_over_ranks(world, win):
+    """bench.py's cfg5 sharding over `world` gloo ranks: every rank computes the same cost bounds
+    (library call), the slices partition the due window, each rank's encoder cost is within one
+    request of the ideal share, and the gathered table -- hence the ISRTF batch -- is the
+    single-process one on every rank."""
+    import bench
+    from oracle.select import isrtf_select
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, win, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    F, due = 65536, -(-65536 // inputs.WINDOW_K)
+    Lt = np.asarray(inputs.trace_lengths(F, seed=0)[0], np.int32)
+    slots = bench.due_windows(F, due)[win]
+    bounds = [r[1] for r in res]
+    assert all(bb == bounds[0] for bb in bounds)
+    assert sorted(s for r in res for s in r[2]) == sorted(slots.tolist())  # a partition of the window
+    L = Lt[slots].astype(np.float64)
+    cost = 169.87e6 * L + 36864.0 * L * L
+    share = [cost[bounds[0][r]:bounds[0][r + 1]].sum() for r in range(world)]
+    assert max(share) - cost.sum() / world <= cost.max()
+    pred_all = inputs.random_predictions(F, seed=win)
+    table = np.zeros(F, np.float32)
+    table[slots] = pred_all[slots]
+    gen, order, running = inputs.random_sched_state(F, seed=win)
+    ids, cnt, _, _ = isrtf_select(table, gen, 256, 0, True, order, running)
+    for r in res:
+        assert r[3] == ids[:cnt].tolist()
+        np.testing.assert_array_equal(np.asarray(r[4], np.float32), table[slots])  # NaN slots included
