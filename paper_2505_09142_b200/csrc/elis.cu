@@ -551,11 +551,12 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
   // (FFN2 2.13 vs 2.10 ms per cfg2 step, scripts/_ab_gx.sh) -- the long-K GEMM is bound by operand
   // traffic, not by the SM count
   const bool gx_on = getenv("ELIS_GEMM_GX") && getenv("ELIS_GEMM_GX")[0] == '1';
+  const bool gx_out = getenv("ELIS_GEMM_GX_OUT") && getenv("ELIS_GEMM_GX_OUT")[0] == '1';
   // M-tile order alternates along the layer chain (L2 reuse of the A rows the producer wrote last):
   // QKV and FFN1 run descending.  Measured 8.12 -> 8.01 ms per cfg2 step (scripts/_ab_zigzag.sh);
   // ELIS_GEMM_ZIGZAG=0 restores ascending order everywhere
   const bool zigzag = !(getenv("ELIS_GEMM_ZIGZAG") && getenv("ELIS_GEMM_ZIGZAG")[0] == '0');
-  if ((cfg->residual_stream == ELIS_RESID_FP16) && gx_on) {
+  if ((cfg->residual_stream == ELIS_RESID_FP16) && (gx_on || gx_out)) {
     const size_t mt = (static_cast<size_t>(T) + 255) / 256;
     ALLOC(p->gx_stats, mt * (cfg->hidden / 256) * 2 * 128);
     ALLOC(p->gx_flag, mt * 2);
@@ -599,6 +600,13 @@ elis_status elis_predictor_create(const elis_config* cfg, const float* weights, 
       L.p_ffn2.args.gstats = p->gx_stats;
       L.p_ffn2.args.gflag = p->gx_flag;
       L.p_ffn2.args.err = p->err;
+    }
+    // ELIS_GEMM_GX_OUT=1: the same global-memory statistics exchange for the out-projection (its CTA
+    // pairs on every SM instead of 132 SMs in clusters of 6); shares FFN2's buffers (same stream)
+    if ((cfg->residual_stream == ELIS_RESID_FP16) && gx_out) {
+      L.p_out.args.gstats = p->gx_stats;
+      L.p_out.args.gflag = p->gx_flag;
+      L.p_out.args.err = p->err;
     }
     if (!ok) return cleanup_fail(ELIS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   }

@@ -793,6 +793,7 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
     switch (g.epi) {
       case EPI_BIAS_RESID16_LN:
         if (deep && g.args.gstats) return launch_bn<256, EPI_BIAS_RESID16_LN, true, 2, true>(g, num_sms, st);
+        if (g.args.gstats) return launch_bn<256, EPI_BIAS_RESID16_LN, false, 2, true>(g, num_sms, st);
         return deep ? launch_bn<256, EPI_BIAS_RESID16_LN, true, 2>(g, num_sms, st)
                     : launch_bn<256, EPI_BIAS_RESID16_LN, false, 2>(g, num_sms, st);
       case EPI_BIAS_BF16: return launch_bn<256, EPI_BIAS_BF16, false, 2>(g, num_sms, st);
