@@ -617,6 +617,20 @@ __global__ void __launch_bounds__(128, 4)
 // and V_{j+1} into V_{j-1}'s (S_j's completion implies PV_{j-1}'s).  Measured (A/B, one session,
 // profiles/r02_ab_attention_64key.txt): cfg2 attention 1.58 / 1.53 vs 1.60 / 1.54 ms per step,
 // cfg5 8.42 vs 8.58 ms; ELIS_ATTN_ENGINE=128 selects the 128-key engine above.
+// MMA issue in the 64-key engine: 1 (default) = warp 0 converged with one lane elected in the asm,
+// 0 = thread 0 alone (per-operand uniform-register broadcasts around every MMA)
+#ifndef ELIS_ATTN_WARP_ISSUE
+#define ELIS_ATTN_WARP_ISSUE 1
+#endif
+#if ELIS_ATTN_WARP_ISSUE
+#define ATTN_MMA_SS tc_mma_f16_w
+#define ATTN_MMA_TS tc_mma_f16_tmem_a_w
+#define ATTN_COMMIT tc_commit_w
+#else
+#define ATTN_MMA_SS tc_mma_f16
+#define ATTN_MMA_TS tc_mma_f16_tmem_a
+#define ATTN_COMMIT tc_commit
+#endif
 constexpr int TKB64 = 64;
 constexpr int kBlk64 = TKB64 * TD * 2;                        // 8 KB
 constexpr int kAttn64Smem = kBlkBytes + 4 * kBlk64 + 1024 + 256;  // Q, K[2], V[2]
@@ -691,15 +705,16 @@ __global__ void __launch_bounds__(128, 4)
   constexpr uint32_t idesc_o = (F16 ? make_idesc_f16_f32(TQ, TD) : make_idesc_bf16_f32(TQ, TD)) | (1u << 16);
   const uint64_t dq = make_sw128_desc(smem_u32(sQ));
   ATR(2);  // setup done (barriers, TMEM)
-  if (issuer) {  // S_0
+  if (ELIS_ATTN_WARP_ISSUE ? warp == 0 : issuer) {  // S_0 (MMAs: warp 0 converged, one lane elected)
     mbar_wait(q_full, 0);
     mbar_wait(&k_full[0], 0);
     ATR(3);  // Q, K_0, V_0 loaded
+    if (ELIS_ATTN_WARP_ISSUE) __syncwarp();  // the elect.sync in the MMA issue needs the whole warp converged
     tc_fence_after();
     const uint64_t dk = make_sw128_desc(smem_u32(sK));
 #pragma unroll
-    for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
-    tc_commit(s_full);
+    for (int k = 0; k < TD / 16; ++k) ATTN_MMA_SS(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+    ATTN_COMMIT(s_full);
   }
   float m = 0.f, l = 0.f;
   const unsigned long long sc2 = f2_pack(scale_log2, scale_log2);
@@ -817,26 +832,28 @@ __global__ void __launch_bounds__(128, 4)
     tc_fence_before();
     __syncthreads();  // P_j complete in TMEM (all 128 rows)
     ATR(7);  // all warps' P_j in TMEM
-    if (issuer) {
+    if (ELIS_ATTN_WARP_ISSUE ? warp == 0 : issuer) {
       tc_fence_after();
       const int b = j & 1;
       mbar_wait(&v_full[b], (j >> 1) & 1);
       ATR(8);  // V_j (and K_j) loaded
+      if (ELIS_ATTN_WARP_ISSUE) __syncwarp();  // the elect.sync in the MMA issue needs the whole warp converged
       const int nks = (nk + 15) / 16;  // 16-key steps holding valid keys
       for (int ks = 0; ks < nks; ++ks) {
         const uint64_t dv = make_sw128_desc(smem_u32(sV + b * kBlk64 + ks * (16 * TD * 2)));
-        tc_mma_f16_tmem_a(tmem + kOCol, tmem + ks * 8, dv, idesc_o, (j | ks) != 0 ? 1u : 0u);
+        ATTN_MMA_TS(tmem + kOCol, tmem + ks * 8, dv, idesc_o, (j | ks) != 0 ? 1u : 0u);
       }
       if (j + 1 < nkb) {  // S_{j+1} right behind PV_j (in issue order: P_j is read before S overwrites it)
         const int b1 = (j + 1) & 1;
         mbar_wait(&k_full[b1], ((j + 1) >> 1) & 1);
+        if (ELIS_ATTN_WARP_ISSUE) __syncwarp();  // the elect.sync in the MMA issue needs the whole warp converged
         tc_fence_after();
         const uint64_t dk = make_sw128_desc(smem_u32(sK + b1 * kBlk64));
 #pragma unroll
-        for (int k = 0; k < TD / 16; ++k) tc_mma_f16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
-        tc_commit(s_full);
+        for (int k = 0; k < TD / 16; ++k) ATTN_MMA_SS(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0);
+        ATTN_COMMIT(s_full);
       } else {
-        tc_commit(o_full);
+        ATTN_COMMIT(o_full);
       }
     }
   }

@@ -183,6 +183,46 @@ template <uint32_t NCOLS>
 ELIS_DEV void tmem_dealloc_pair(uint32_t base) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(NCOLS) : "memory");
 }
+// The same MMAs / commit issued by a whole converged warp with one lane elected inside the asm: the
+// operands stay warp-uniform values, so no per-operand R2UR broadcast / elect loop is generated
+// around each UTCHMMA (single-thread issue measured ~55 cycles per small MMA, warp-elect issue 30.5 =
+// the pipe rate for M 128 N 64 TS; scripts/tc_rate.cu, profiles/r02zj_tc_rate_elect.txt)
+ELIS_DEV void tc_mma_f16_w(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 r;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+ELIS_DEV void tc_mma_f16_tmem_a_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc,
+                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 r;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+ELIS_DEV void tc_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      ".reg .b32 r;\n"
+      "elect.sync r|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 ELIS_DEV void tc_mma_f16_pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
