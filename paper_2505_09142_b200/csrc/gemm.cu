@@ -789,6 +789,13 @@ cudaError_t launch_gemm(const GemmPlan& g, int num_sms, cudaStream_t st) {
     }
   }
   if (g.f16) {  // fp16 operands and 16-bit outputs
+    if (g.bn128) {  // small-M plans (gemm_plan_bn128)
+      switch (g.epi) {
+        case EPI_BIAS_BF16: return launch_bn<128, EPI_BIAS_BF16, false, 2>(g, num_sms, st);
+        case EPI_BIAS_GELU_BF16: return launch_bn<128, EPI_BIAS_GELU_BF16, false, 2>(g, num_sms, st);
+        default: return cudaErrorInvalidValue;
+      }
+    }
     if (!b256) return cudaErrorInvalidValue;
     switch (g.epi) {
       case EPI_BIAS_RESID16_LN:
@@ -935,6 +942,13 @@ bool make_gemm_plan_f8(GemmPlan* g, const void* A, uint64_t a_rows, const void* 
     g->tmR = g->tmO;
     g->tmOb = g->tmO;
   }
+  return true;
+}
+
+bool gemm_plan_bn128(GemmPlan* g, const void* W) {
+  if (!g->f16 || g->f8 || (g->epi != EPI_BIAS_BF16 && g->epi != EPI_BIAS_GELU_BF16)) return false;
+  if (!make_tmap_bf16_kmajor(&g->tmB, W, g->args.N, g->args.K, 128 / 2)) return false;
+  g->bn128 = 1;
   return true;
 }
 

@@ -61,7 +61,11 @@ struct GemmPlan {
   int epi;
   int f8;            // operands E4M3 (kind::f8f6f4): A [M, K] / W [N, K] bytes, 128-element K blocks
   int f16;           // operands fp16 (kind::f16, A/B format f16); 16-bit outputs written as fp16
+  int bn128 = 0;     // fp16 bias / GELU epilogues: 256 x 128 pair tiles (twice the tiles of a small M)
 };
+// A copy of an fp16 bias / GELU plan for 256 x 128 pair tiles (W boxes of 64 rows).  Each output
+// element is the same sum of the same MMAs in the same K order as with 256 x 256 tiles.
+bool gemm_plan_bn128(GemmPlan* g, const void* W);
 // bf16 output in head-major planes: out[N/64][rows][64] (the QKV projection feeding attention:
 // every (head, 128-token) box of Q, K or V is one contiguous 16 KB block)
 bool gemm_plan_set_head_major(GemmPlan* g, void* out, uint64_t rows);
