@@ -478,5 +478,21 @@ inline void pdl_attr(cudaLaunchAttribute& a) {
   a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a.val.programmaticStreamSerializationAllowed = 1;
 }
+// A plain (non-cluster) launch configuration carrying the attribute when PDL is enabled.
+inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, cudaStream_t st, size_t smem = 0) {
+  static cudaLaunchAttribute attr = [] {
+    cudaLaunchAttribute a{};
+    pdl_attr(a);
+    return a;
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cfg;
+}
 
 }  // namespace elis
